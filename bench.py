@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the MemShare KV-block reuse path on B200 (BASELINE.json metric:
+"candidate KV-block pairs scored/s and HBM GB/s (% of peak) at 1/2/4/8 B200").
+
+One STEP = one full pass of the hot path (a1 segment -> a2-a4 Stage 1 + pairs -> a5-a6 block
+distance + selection -> a7 remap) over one batch (configs[1] = "c2": one 12,406-token
+synthetic CoT with DeepSeek-R1-Distill-Qwen-32B's KV shape) per GPU. Before each step the block
+table / refcounts / free list are restored from a pristine device copy (a few KB), so every step
+does identical work. Inputs are resident in HBM; the 3.25 GB KV pool (1.38 GB of distinct blocks
+read per step) is far larger than the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "candidate KV-block pairs scored/s"
+UNIT = "pairs/s"
+GPU_LAUNCHES_PER_STEP = 7     # seg_count, seg_fill, encode, stage1, fill, distance, remap
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c2", choices=["c2", "tiny", "c3", "c4"])
+    ap.add_argument("--seqs-per-gpu", type=int, default=0, help="c3/c4: sequences per GPU (0 = config default)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="seq", choices=["seq", "headshard"])
+    ap.add_argument("--seed", type=int, default=int(os.environ.get("MEMSHARE_SEED", "0")))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def make_workload(cfg, seed, rank, seqs):
+    from synth import workloads
+    if cfg == "c2":
+        return workloads.c2(seed=seed + rank)
+    if cfg == "tiny":
+        return workloads.tiny(eta=0.05)
+    if cfg == "c3":
+        return workloads.c3(num_seqs=seqs or 8, seed=seed, first_seq=rank * (seqs or 8))
+    if cfg == "c4":
+        return workloads.c4(num_seqs=seqs or 8, seed=seed + rank)
+    raise ValueError(cfg)
+
+
+def describe(cfg, w, world, mode):
+    sh = w.shape
+    return {"workload": {"c2": "configs[1]: DeepSeek-R1-Distill-Qwen-32B KV shape, 1 x 12,406-token synthetic CoT "
+                                "per GPU (128-token prompt, MATH-500-like planted redundancy)",
+                         "tiny": "configs[0]: tiny T0 fixture",
+                         "c3": "configs[2]: QwQ-32B KV shape, 12,288-token CoTs",
+                         "c4": "configs[3]: Phi-4-reasoning-plus KV shape, AIME-length traces"}[cfg],
+            "kv_shape": {"layers": sh.num_layers, "kv_heads": sh.num_kv_heads, "head_dim": sh.head_dim,
+                         "block_size": sh.block_size, "kv_dtype": "bf16"},
+            "seqs_per_gpu": w.batch.num_seqs, "tokens_per_gpu": w.num_tokens, "tau_s": w.tau_s,
+            "tau_b": round(w.tau_b, 6), "eta": w.eta, "pairing": "aligned", "stage1": "offline (every step current)",
+            "parallelism": (f"seq-shard dp{world}" if mode == "seq" else f"kv-head-shard hs{world}"),
+            "l2": "inputs larger than L2 (pool %.2f GB/GPU vs 126 MB L2); no flush" % (w.pool_bytes() / 1e9)}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
+                                       "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        self.t0 = self.t1 = None
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        inwin = [r for r in rows if self.t0 - 1 <= r[0] <= self.t1 + 1] or rows
+        if not inwin:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in inwin for i, x in enumerate(r[3]) if x.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[1] for r in inwin])), "sm_max_mhz": max(r[2] for r in inwin),
+                "reasons": reasons, "samples": len(inwin)}
+
+
+# ----------------------------------------------------------------------------- oracle
+def oracle_pass(w, kh, vh, ls, bs, npairs_limit=None):
+    """The oracle as it stands on the host: a1-a4, a5-a6 on (a prefix of) the pairs, a7."""
+    import oracle
+    b, sh = w.batch, w.shape
+    t0 = time.perf_counter()
+    st = oracle.segment_steps(b.tokens, b.seq_tok_off, b.gen_start, b.final, b.delim_ids)
+    oc = oracle.step_candidates(b.tokens, b.seq_tok_off, st, b.delim_ids, w.table, sh.block_size, w.tau_s)
+    t1 = time.perf_counter()
+    pr = oc["pairs"]
+    P = pr["seq"].size if npairs_limit is None else min(npairs_limit, pr["seq"].size)
+    D = oracle.block_distance(kh, vh, ls, bs, sh.num_layers, sh.num_kv_heads, sh.num_kv_heads, sh.head_dim,
+                              sh.block_size, pr["target_phys"][:P], pr["source_phys"][:P])
+    toff = oc["target_off"]
+    T = int(np.searchsorted(toff, P, side="right") - 1) if npairs_limit is not None else toff.size - 1
+    best, acc, _ = oracle.select(D, toff[:T + 1], pr["source_logical"][:P], w.tau_b)
+    dec = oracle.decisions({k: v[:P] for k, v in pr.items()}, toff[:T + 1], D, best, acc)
+    t2 = time.perf_counter()
+    oracle.remap(w.table, w.refcount, w.free_list, w.free_count, dec, sh.block_size)
+    t3 = time.perf_counter()
+    return {"pairs": P, "t_front": t1 - t0, "t_stage2": t2 - t1, "t_remap": t3 - t2, "t_total": t3 - t0}
+
+
+def host_cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (this tier's reference arm), as it stands, on host cores."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    w = make_workload(args.config, args.seed, 0, args.seqs_per_gpu)
+    k, v, ls, bs = w.host_pool()
+    sh = w.shape
+    st = oracle.segment_steps(w.batch.tokens, w.batch.seq_tok_off, w.batch.gen_start, w.batch.final, w.batch.delim_ids)
+    oc = oracle.step_candidates(w.batch.tokens, w.batch.seq_tok_off, st, w.batch.delim_ids, w.table, sh.block_size,
+                                w.tau_s)
+    pr, toff = oc["pairs"], oc["target_off"]
+    T = toff.size - 1
+    # calibrate: seconds per target group (a5-a6 on all pairs of a target)
+    t0 = time.perf_counter()
+    one = oracle.block_distance(k, v, ls, bs, sh.num_layers, sh.num_kv_heads, sh.num_kv_heads, sh.head_dim,
+                                sh.block_size, pr["target_phys"][:4], pr["source_phys"][:4])
+    per_pair = (time.perf_counter() - t0) / 4
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    n_t = max(1, min(T, int(budget / (per_pair * max(1.0, pr["seq"].size / max(T, 1))))))
+    cursor = 0
+    times, pairs_done = [], []
+    for it in range(args.warmup + args.steps):
+        ts = [(cursor + i) % T for i in range(n_t)]
+        cursor = (cursor + n_t) % T
+        sel = np.concatenate([np.arange(toff[t], toff[t + 1]) for t in ts])
+        sub_off = np.concatenate([[0], np.cumsum([toff[t + 1] - toff[t] for t in ts])])
+        t0 = time.perf_counter()
+        D = oracle.block_distance(k, v, ls, bs, sh.num_layers, sh.num_kv_heads, sh.num_kv_heads, sh.head_dim,
+                                  sh.block_size, pr["target_phys"][sel], pr["source_phys"][sel])
+        oracle.select(D, sub_off, pr["source_logical"][sel], w.tau_b)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            pairs_done.append(sel.size)
+    total_t = float(np.sum(times))
+    value = float(np.sum(pairs_done)) / total_t
+    sample = (f"a5-a6 (oracle_block_distance + oracle_select, fp64, 1 thread) on {n_t} target group(s) "
+              f"(~{np.mean(pairs_done):.1f} pairs) per step, rotating over the {pr['seq'].size} pairs of the "
+              f"{args.config} workload; a1-a4/a7 excluded from the steps")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": describe(args.config, w, 1, "seq"),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": host_cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2507_21433_b200 import _lib as L
+    from paper_2507_21433_b200.pipeline import MemSharePath
+
+    w = make_workload(args.config, args.seed, rank if args.mode == "seq" else 0, args.seqs_per_gpu)
+    sh = w.shape
+    h_local, h_off = sh.num_kv_heads, 0
+    if args.mode == "headshard":
+        per = -(-sh.num_kv_heads // world)
+        h_off = min(rank * per, sh.num_kv_heads)
+        h_local = max(1, min(per, sh.num_kv_heads - h_off))
+    k, v, ls, bs = w.device_pool(dev, h_local=h_local, head_offset=h_off)
+    b = w.batch
+    path = MemSharePath(b.tokens, b.seq_tok_off, b.gen_start, b.final, b.delim_ids, w.table, w.refcount, w.free_list,
+                        w.free_count, k, v, ls, bs, w.num_blocks, sh.num_layers, h_local, sh.num_kv_heads,
+                        sh.head_dim, sh.block_size, device=dev)
+    counts = path.autosize(w.tau_s)
+    if args.mode == "headshard":
+        path.alloc_partial()
+    torch.cuda.synchronize()
+    pristine = {n: getattr(path, n).clone() for n in ("table", "refcount", "free_list", "free_count")}
+    stream = path.stream
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def restore():
+        for n, t in pristine.items():
+            getattr(path, n).copy_(t, non_blocking=True)
+
+    def step(d_ev=None):
+        restore()
+        path.segment()
+        path.candidates(w.tau_s)
+        if d_ev is not None:
+            d_ev[0].record(stream)
+        if args.mode == "headshard":
+            path.distance_call(w.tau_b, L.DIST_PARTIAL)
+            n = counts["pairs"] * sh.num_layers * 2
+            if world > 1:
+                dist.all_reduce(path.partial_sq[:n])
+            path.distance_call(w.tau_b, L.DIST_FINALIZE)
+        else:
+            path.distance_call(w.tau_b)
+        if d_ev is not None:
+            d_ev[1].record(stream)
+        path.remap()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert path.read_status() == 0, f"device status {L.status_string(path.read_status())}"
+    # distinct physical blocks per step (algorithmic bytes of the distance kernel)
+    pr = path.read_candidates()["pairs"]
+    U = int(np.unique(np.concatenate([pr["target_phys"], pr["source_phys"]])).size)
+    P, T = counts["pairs"], counts["targets"]
+    slice_b = sh.block_size * h_local * sh.head_dim * 2
+    blk_b = sh.num_layers * 2 * slice_b
+    kv_bytes = U * blk_b
+    meta_bytes = P * (24 + 4 + 1) + T * (8 + 32)
+    alg_bytes = kv_bytes + meta_bytes
+
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+    d_events = [(ev(), ev()) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark_start()
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(d_events[i])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark_end()
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    d_ms = float(np.mean([a.elapsed_time(b_) for a, b_ in d_events]))
+    ck = clocks.stop()
+    assert path.read_status() == 0
+
+    # max over ranks of the step time; sum of pairs over ranks
+    t = torch.tensor([ms_total, float(P)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        ms_total, pairs_all = float(tmax[0]), float(t[1])
+    else:
+        pairs_all = float(P)
+    if args.mode == "headshard":
+        pairs_all = float(P)             # every rank scores the same pairs (strong scaling)
+    ms_step = ms_total / args.steps
+    value = pairs_all / (ms_step / 1e3)
+
+    # ---------------------------------------------------------------- e2e through the public API
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda x: torch.as_tensor(np.ascontiguousarray(x)).pin_memory()
+        h_in = {"tokens": pin(b.tokens.astype(np.int32)), "seq_tok_off": pin(b.seq_tok_off.astype(np.int64)),
+                "gen_start": pin(b.gen_start.astype(np.int32)), "final": pin(b.final.astype(np.uint8)),
+                "table": pin(w.table.astype(np.int32).ravel()), "refcount": pin(w.refcount.astype(np.int32)),
+                "free_list": pin(w.free_list.astype(np.int32)), "free_count": pin(np.asarray([w.free_count], np.int64))}
+        h2d = sum(x.numel() * x.element_size() for x in h_in.values())
+        out_dec = torch.empty(path.decisions.numel(), dtype=torch.uint8).pin_memory()
+        out_tab = torch.empty(path.table.numel(), dtype=torch.int32).pin_memory()
+        out_cnt = torch.empty(5, dtype=torch.int64).pin_memory()
+        d2h = out_dec.numel() + out_tab.numel() * 4 + out_cnt.numel() * 8
+        cnt_dev = torch.empty(5, dtype=torch.int64, device=dev)
+
+        def e2e_step():
+            for n, x in h_in.items():
+                getattr(path, n).copy_(x, non_blocking=True)
+            path.segment()
+            path.candidates(w.tau_s)
+            if args.mode == "headshard":
+                path.distance_call(w.tau_b, L.DIST_PARTIAL)
+                if world > 1:
+                    dist.all_reduce(path.partial_sq[:counts["pairs"] * sh.num_layers * 2])
+                path.distance_call(w.tau_b, L.DIST_FINALIZE)
+            else:
+                path.distance_call(w.tau_b)
+            path.remap()
+            torch.cat([path.num_pairs, path.num_targets, path.num_freed, path.affected, path.free_count],
+                      out=cnt_dev)
+            out_dec.copy_(path.decisions, non_blocking=True)
+            out_tab.copy_(path.table, non_blocking=True)
+            out_cnt.copy_(cnt_dev, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        for _ in range(max(3, args.warmup // 4)):
+            e2e_step()
+        n_e2e = max(10, min(args.steps, 200))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a0, a1 = ev(), ev()
+        a0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a0.elapsed_time(a1) / n_e2e
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te[0])
+        assert int(out_cnt[0]) == P
+        e2e = {"value": pairs_all / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms, "steps": n_e2e,
+               "note": "public API (MemSharePath over the C ABI); per step: pinned H2D of tokens/offsets/table/"
+                       "refcounts/free list, the 4 calls, D2H of decisions/table/counters, stream sync; the KV pool "
+                       "is the device-resident serving cache"}
+
+    # ---------------------------------------------------------------- cpu baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        kh = path.k_pool.view(torch.int16).cpu().numpy().view(np.uint16)
+        vh = path.v_pool.view(torch.int16).cpu().numpy().view(np.uint16)
+        r = oracle_pass(w, kh, vh, ls, bs)
+        cpu = {"value": r["pairs"] / r["t_total"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": (f"one full oracle pass (a1-a7, fp64, single thread) over the {args.config} workload: "
+                          f"{r['pairs']} pairs; front {r['t_front']:.2f}s, stage2 {r['t_stage2']:.2f}s, "
+                          f"remap {r['t_remap']:.3f}s"), "cpu": host_cpu_model(), "host_cores": os.cpu_count()}
+
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (d_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_distance_{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak" if args.mode == "seq" else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": describe(args.config, w, world, args.mode),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "distance_kernel (memshare_block_distance)",
+                     "kernel_ms": d_ms, "kernel_share_of_step": d_ms / ms_step, "algorithmic_bytes": alg_bytes,
+                     "kv_bytes": kv_bytes, "distinct_blocks": U, "peak_source": peak_src,
+                     "frac_of_nominal_8000": achieved / 8000.0},
+        "per_step": {"pairs": P, "targets": T, "steps": counts["steps"], "matches": counts["matches"],
+                     "freed_blocks": int(path.num_freed.item()), "affected_tokens": int(path.affected.item())},
+        "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
+        "clocks": {"sm_mhz": ck["sm_mhz"], "sm_max_mhz": ck["sm_max_mhz"], "reasons": ck["reasons"],
+                   "samples": ck["samples"]},
+        "e2e": e2e, "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,237 @@
+/* memshare.h -- C ABI of the B200-native MemShare KV-block reuse path (arXiv 2507.21433).
+ *
+ * Four calls, one per step of the path:
+ *   memshare_segment_steps    a1   split token traces into reasoning steps
+ *   memshare_step_candidates  a2-a4 Stage 1 bag-of-words cosine filter and the  PAPER.md:224-234,
+ *                                  candidate KV-block pair list                 :252-264, :267, :319
+ *   memshare_block_distance   a5-a6 Stage 2 normalized block distance, the      PAPER.md:237-248,
+ *                                  threshold and the per-target selection       :267-269, :319-320
+ *   memshare_remap            a7   zero-copy sharing: block-table rewrite,
+ *                                  refcounts, free list
+ *
+ * Conventions (all calls):
+ *  - Pointers named *_host are host memory; every other pointer is DEVICE memory (cudaMalloc /
+ *    torch CUDA tensors). The caller owns every buffer; the library keeps no device memory
+ *    between calls. Scratch comes from `workspace` (device, >= the matching *_workspace_size()
+ *    bytes, 256-byte aligned); it need not be initialised and may be reused after the call's
+ *    stream work completes.
+ *  - `stream` is a cudaStream_t passed as void*. Every call validates its host-visible
+ *    arguments, then only ENQUEUES work on `stream` and returns: no host synchronisation, no
+ *    allocation. Counts produced on the device (num_pairs, num_targets, ...) stay on the device
+ *    and later calls read them there, so a whole round runs without a host round trip and can be
+ *    captured in a CUDA graph.
+ *  - Host-detectable errors return MEMSHARE_ERR_INVALID_ARGUMENT and enqueue nothing. A launch
+ *    failure returns MEMSHARE_ERR_CUDA.
+ *  - Device-detected errors are written to `*device_status` (int32, device, sticky: the first
+ *    error wins; the caller zeroes it before the first call):
+ *      MEMSHARE_ERR_CAPACITY   an output exceeded its capacity; the count still holds the
+ *                              required size and writes past the capacity were dropped, so the
+ *                              caller can re-size and re-run (count-then-fill);
+ *      MEMSHARE_ERR_CORRUPTION an id out of range, a refcount underflow, a full free list.
+ *  - Outputs are bit-reproducible run to run on the same GPU for the same inputs.
+ *  - Layout of the paged KV pool (memshare_kv_pool): bf16; the (layer l, physical block b)
+ *    slice of K is the contiguous [d][h_local][d_h] array at k + l*layer_stride + b*block_stride
+ *    (element strides; the vLLM-style layer-major pool has block_stride = d*h_local*d_h and
+ *    layer_stride = num_blocks*block_stride); V likewise. Bases and strides must be 16-byte
+ *    aligned and d_h % 8 == 0.
+ */
+#ifndef MEMSHARE_H
+#define MEMSHARE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MEMSHARE_ABI_VERSION 1
+
+typedef int32_t memshare_status;
+#define MEMSHARE_OK 0
+#define MEMSHARE_ERR_INVALID_ARGUMENT 1
+#define MEMSHARE_ERR_CAPACITY 2
+#define MEMSHARE_ERR_CORRUPTION 3
+#define MEMSHARE_ERR_CUDA 4
+
+/* Which steps are CURRENT (compared against their history) in memshare_step_candidates.
+ * ALL = offline, every finished step; LAST = online, the last finished step of each sequence
+ * ("for each decoding step"); RANGE = local steps [cur_begin[s], cur_end[s]). */
+#define MEMSHARE_CUR_ALL 0
+#define MEMSHARE_CUR_LAST 1
+#define MEMSHARE_CUR_RANGE 2
+
+/* Block pairing between a current step k and a candidate step j (reading R14):
+ * ALIGNED = i-th full block of k with the i-th full block of j ("corresponding");
+ * CROSS = every full block of k with every full block of j ("pairwise"). */
+#define MEMSHARE_PAIR_ALIGNED 0
+#define MEMSHARE_PAIR_CROSS 1
+
+/* memshare_block_distance modes: FULL streams the pool and finalizes; PARTIAL streams the
+ * pool and writes per-(pair, layer) squared sums for a cross-rank all-reduce (KV-head-sharded
+ * mode); FINALIZE reads the (all-reduced) squared sums and finalizes without the pool. */
+#define MEMSHARE_DIST_FULL 0
+#define MEMSHARE_DIST_PARTIAL 1
+#define MEMSHARE_DIST_FINALIZE 2
+
+#define MEMSHARE_MAX_DELIMS 16
+
+/* KV geometry. num_kv_heads_global is the h of Alg. 1's 2dh normaliser (reading R17); the pool
+ * holds num_kv_heads_local of them (== global unless head-sharded). */
+typedef struct memshare_dims {
+  int32_t num_layers;          /* N, 1..256 */
+  int32_t num_kv_heads_local;  /* heads stored in this pool */
+  int32_t num_kv_heads_global; /* h in (Delta_K + Delta_V)/(2dh) */
+  int32_t head_dim;            /* d_h, multiple of 8 */
+  int32_t block_size;          /* d, tokens per block (reading R18) */
+} memshare_dims;
+
+typedef struct memshare_kv_pool {
+  const void* k;        /* bf16, device */
+  const void* v;        /* bf16, device */
+  int64_t layer_stride; /* elements */
+  int64_t block_stride; /* elements */
+  int32_t num_blocks;   /* physical blocks addressable through this pool */
+  int32_t reserved;
+} memshare_kv_pool;
+
+/* One Stage-1 survivor: step `cand_step` of sequence `seq` is a candidate of current step
+ * `step` (local step indices), `rank`-th by (cosine desc, cand_step asc). 24 bytes. */
+typedef struct memshare_step_match {
+  int32_t seq, step, cand_step, rank;
+  double cosine;
+} memshare_step_match;
+
+/* One candidate KV-block pair: logical blocks of `seq` and their physical ids as read from the
+ * block table at call time; pairs are grouped by target (target_idx ascending = ascending
+ * (seq, target_logical)), sources ascending by logical. 24 bytes. */
+typedef struct memshare_block_pair {
+  int32_t seq, target_idx, target_logical, source_logical, target_phys, source_phys;
+} memshare_block_pair;
+
+/* One per target: the minimal-distance source (ties -> smaller source_logical) and whether it
+ * is reused (distance < tau_b). 32 bytes. */
+typedef struct memshare_decision {
+  int32_t seq, target_logical, target_phys, source_logical, source_phys, accepted;
+  float distance;
+  int32_t num_candidates;
+} memshare_decision;
+
+/* ---------------------------------------------------------------------------------------- a1
+ * Step segmentation (steps "separated by delimiters like \n\n").
+ * A step ends at token i when t[i] is a delimiter and t[i+1] is not (the delimiter run belongs
+ * to the step it ends), or at the last token of a FINAL sequence; tokens before gen_start[s]
+ * are the prompt. Only finished steps are emitted; an open tail is not a step (reading R3).
+ *   tokens        int32 [seq_tok_off[num_seqs]]   concatenated token ids of all sequences
+ *   seq_tok_off   int64 [num_seqs+1]             sequence s = tokens[seq_tok_off[s] .. [s+1])
+ *   gen_start     int32 [num_seqs]               first generated position of each sequence
+ *   seq_final     uint8 [num_seqs]               1 = sequence finished
+ *   delim_ids_host int32 [num_delims] (host)     1..MEMSHARE_MAX_DELIMS delimiter token ids
+ * Outputs (global step index g = seq_step_off[s] + local step m):
+ *   step_start/step_end int32 [step_cap]         [start, end) relative to the sequence start
+ *   step_nbag     int32 [step_cap]               content (non-delimiter) tokens of the step
+ *   seq_step_off  int64 [num_seqs+1]             always written in full (the required size is
+ *                                                seq_step_off[num_seqs]; CAPACITY if > step_cap)
+ * Errors: INVALID_ARGUMENT for null pointers, num_seqs < 0, num_delims outside 1..16, step_cap
+ * < 0, a short workspace. */
+memshare_status memshare_segment_steps(const int32_t* tokens, const int64_t* seq_tok_off, const int32_t* gen_start,
+                                       const uint8_t* seq_final, int32_t num_seqs, const int32_t* delim_ids_host,
+                                       int32_t num_delims, int32_t* step_start, int32_t* step_end,
+                                       int32_t* step_nbag, int64_t* seq_step_off, int64_t step_cap, void* workspace,
+                                       size_t workspace_bytes, int32_t* device_status, void* stream);
+size_t memshare_segment_steps_workspace_size(int32_t num_seqs);
+
+/* ------------------------------------------------------------------------------------- a2-a4
+ * Stage 1 + candidate block pairs (Alg. 1 Stage 1; "bag-of-words",
+ * PAPER.md:254; threshold "exceeding"; "their corresponding KV cache blocks",
+ * PAPER.md:267).
+ * For every CURRENT non-void step k of sequence s (cur_mode) and every earlier non-void step j of
+ * the same sequence: dot = <c_k, c_j> over the content-token count vectors (int64, exact),
+ * cos = (double)dot / sqrt((double)|c_k|^2 * (double)|c_j|^2) (IEEE round-to-nearest, no
+ * contraction); j survives iff cos > tau_s; survivors ordered (cos desc, j asc), the first top_k
+ * kept (0 = all). Each survivor yields block pairs between the full blocks
+ * F = [ceil(start/d), floor(end/d)) of k (targets) and of j (sources), ALIGNED or CROSS; physical
+ * ids come from block_table AS GIVEN (snapshot); per target, a source whose physical id repeats
+ * is dropped (the smaller logical is kept).
+ *   tokens, num_tokens, seq_tok_off, num_seqs       as for memshare_segment_steps
+ *   seq_step_off, step_start, step_end, step_nbag   memshare_segment_steps outputs; step_cap is
+ *                                                    their capacity
+ *   cur_begin/cur_end int32 [num_seqs]              only for MEMSHARE_CUR_RANGE (else NULL)
+ *   block_table   int32 [num_seqs][table_stride]    logical -> physical, entries < num_blocks
+ *   tau_s in [-1, 1]; top_k >= 0; pairing ALIGNED|CROSS; block_size = d
+ * Outputs: matches [match_cap] ordered (seq, step, rank); pairs [pair_cap] grouped by target;
+ *   target_off int64 [target_cap+1] (pairs of target t are [target_off[t], target_off[t+1]));
+ *   num_matches/num_pairs/num_targets int64 (device).
+ * Limits (CAPACITY if exceeded): <= 1024 survivors per current step when top_k == 0 or
+ *   top_k > 512; <= 4096 full blocks per step. */
+memshare_status memshare_step_candidates(
+    const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off, int32_t num_seqs,
+    const int64_t* seq_step_off, const int32_t* step_start, const int32_t* step_end, const int32_t* step_nbag,
+    int64_t step_cap, const int32_t* delim_ids_host, int32_t num_delims, int32_t cur_mode, const int32_t* cur_begin,
+    const int32_t* cur_end, const int32_t* block_table, int32_t table_stride, int32_t num_blocks, int32_t block_size,
+    double tau_s, int32_t top_k, int32_t pairing, memshare_step_match* matches, int64_t match_cap,
+    int64_t* num_matches, memshare_block_pair* pairs, int64_t pair_cap, int64_t* num_pairs, int64_t* target_off,
+    int64_t target_cap, int64_t* num_targets, void* workspace, size_t workspace_bytes, int32_t* device_status,
+    void* stream);
+size_t memshare_step_candidates_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap,
+                                               int64_t match_cap);
+
+/* ------------------------------------------------------------------------------------- a5-a6
+ * Stage 2 block distance, threshold and selection (Alg. 1 Stage 2):
+ *   D = (1/N) * sum_l ( ||K_l[Bt] - K_l[Bs]||_F + ||V_l[Bt] - V_l[Bs]||_F ) / (2 d h_global)
+ * for every pair (Bt = target_phys, Bs = source_phys), bf16 inputs, fp32 accumulation (chains of
+ * <= 64 terms, warp trees, fixed-order cross-warp sums), fp64 finalisation, fp32 result.
+ * under[p] = D_p < tau_b. Per target: the pair of minimal D (exact ties -> smaller
+ * source_logical), accepted = D_best < tau_b.
+ *   pool, dims (host structs)     geometry; pool unused in FINALIZE mode
+ *   pairs, target_off, num_pairs, num_targets   memshare_step_candidates outputs (device);
+ *                                 counts are clamped to pair_cap / target_cap
+ *   mode FULL | PARTIAL | FINALIZE
+ *   partial_sq float [pair_cap][N][2]   PARTIAL: output (sum over local heads of squared
+ *                                 differences, [.][l][0] = K, [.][l][1] = V); FINALIZE: input;
+ *                                 FULL: optional output (may be NULL)
+ *   distance float [pair_cap], under uint8 [pair_cap], decisions [target_cap]: outputs
+ *                                 (FULL and FINALIZE; ignored in PARTIAL and may be NULL)
+ * Errors: INVALID_ARGUMENT for bad geometry/alignment/mode, tau_b < 0 or NaN, a short
+ * workspace; device CORRUPTION for a physical id outside [0, num_blocks). */
+memshare_status memshare_block_distance(const memshare_kv_pool* pool_host, const memshare_dims* dims_host,
+                                        const memshare_block_pair* pairs, const int64_t* target_off,
+                                        const int64_t* num_pairs, const int64_t* num_targets, int64_t pair_cap,
+                                        int64_t target_cap, int32_t mode, float* partial_sq, float tau_b,
+                                        float* distance, uint8_t* under, memshare_decision* decisions,
+                                        void* workspace, size_t workspace_bytes, int32_t* device_status,
+                                        void* stream);
+size_t memshare_block_distance_workspace_size(const memshare_dims* dims_host, int64_t pair_cap, int64_t target_cap);
+
+/* ---------------------------------------------------------------------------------------- a7
+ * Zero-copy remap (PAPER.md:276-278 "the mechanism simply updates the block table", :283-284;
+ * SPEC.md:358-366). Decisions must be strictly ascending in (seq, target_logical) (as
+ * memshare_block_distance emits them; else device INVALID_ARGUMENT and nothing is changed). For
+ * each accepted decision: old = block_table[seq][target_logical], new = source_phys; equal ->
+ * no-op; else the entry becomes new, refcount[new] += 1, refcount[old] -= 1 and
+ * *affected_tokens += block_size. A block is FREED iff it was decremented in this call and its
+ * final refcount is 0; freed ids are appended to free_list[*free_count ...] in ascending order of
+ * their last decrementing decision, *free_count advances and *num_freed = freed count.
+ * No KV byte is read or written (zero-copy).
+ *   block_table int32 [num_seqs][table_stride]; refcount int32 [num_blocks];
+ *   free_list int32 [num_blocks]; free_count, num_freed, affected_tokens int64 (device)
+ *   decisions [target_cap], num_targets int64 (device; clamped to target_cap)
+ * Device CORRUPTION: an id outside its range, a final refcount < 0, a free-list overflow (the
+ * state is then unspecified). */
+memshare_status memshare_remap(int32_t* block_table, int32_t table_stride, int32_t num_seqs, int32_t* refcount,
+                               int32_t num_blocks, int32_t* free_list, int64_t* free_count,
+                               const memshare_decision* decisions, const int64_t* num_targets, int64_t target_cap,
+                               int32_t block_size, int64_t* num_freed, int64_t* affected_tokens, void* workspace,
+                               size_t workspace_bytes, int32_t* device_status, void* stream);
+size_t memshare_remap_workspace_size(int32_t num_blocks, int64_t target_cap);
+
+/* Human-readable name of a status code (static string). */
+const char* memshare_status_string(memshare_status status);
+/* MEMSHARE_ABI_VERSION of the loaded library. */
+int32_t memshare_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MEMSHARE_H */

@@ -1,0 +1,165 @@
+"""ctypes binding of libmemshare.so (include/memshare.h): argument marshalling only.
+
+Every function has the C name without the ``memshare_`` prefix and takes torch CUDA tensors
+(device pointers via ``data_ptr()``) plus plain Python scalars; it returns the status code.
+There is no fallback: if the CUDA library is missing or fails to load, importing this module
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmemshare.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "memshare.h")
+
+OK, INVALID_ARGUMENT, CAPACITY, CORRUPTION, CUDA_ERROR = 0, 1, 2, 3, 4
+CUR_ALL, CUR_LAST, CUR_RANGE = 0, 1, 2
+PAIR_ALIGNED, PAIR_CROSS = 0, 1
+DIST_FULL, DIST_PARTIAL, DIST_FINALIZE = 0, 1, 2
+
+MATCH_DTYPE = np.dtype([("seq", "<i4"), ("step", "<i4"), ("cand_step", "<i4"), ("rank", "<i4"), ("cosine", "<f8")])
+PAIR_DTYPE = np.dtype([("seq", "<i4"), ("target_idx", "<i4"), ("target_logical", "<i4"), ("source_logical", "<i4"),
+                       ("target_phys", "<i4"), ("source_phys", "<i4")])
+DECISION_DTYPE = np.dtype([("seq", "<i4"), ("target_logical", "<i4"), ("target_phys", "<i4"),
+                           ("source_logical", "<i4"), ("source_phys", "<i4"), ("accepted", "<i4"),
+                           ("distance", "<f4"), ("num_candidates", "<i4")])
+assert MATCH_DTYPE.itemsize == 24 and PAIR_DTYPE.itemsize == 24 and DECISION_DTYPE.itemsize == 32
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("num_kv_heads_local", ctypes.c_int32),
+                ("num_kv_heads_global", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("block_size", ctypes.c_int32)]
+
+
+class KVPool(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p), ("layer_stride", ctypes.c_int64),
+                ("block_stride", ctypes.c_int64), ("num_blocks", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class MemShareError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U64, F32, F64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_float,
+                                  ctypes.c_double)
+    L.memshare_segment_steps.argtypes = [P, P, P, P, I32, P, I32, P, P, P, P, I64, P, U64, P, P]
+    L.memshare_segment_steps.restype = I32
+    L.memshare_segment_steps_workspace_size.argtypes = [I32]
+    L.memshare_segment_steps_workspace_size.restype = U64
+    L.memshare_step_candidates.argtypes = ([P, I64, P, I32, P, P, P, P, I64, P, I32, I32, P, P, P, I32, I32, I32, F64,
+                                            I32, I32, P, I64, P, P, I64, P, P, I64, P, P, U64, P, P])
+    L.memshare_step_candidates.restype = I32
+    L.memshare_step_candidates_workspace_size.argtypes = [I64, I32, I64, I64]
+    L.memshare_step_candidates_workspace_size.restype = U64
+    L.memshare_block_distance.argtypes = [P, P, P, P, P, P, I64, I64, I32, P, F32, P, P, P, P, U64, P, P]
+    L.memshare_block_distance.restype = I32
+    L.memshare_block_distance_workspace_size.argtypes = [P, I64, I64]
+    L.memshare_block_distance_workspace_size.restype = U64
+    L.memshare_remap.argtypes = [P, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, P, U64, P, P]
+    L.memshare_remap.restype = I32
+    L.memshare_remap_workspace_size.argtypes = [I32, I64]
+    L.memshare_remap_workspace_size.restype = U64
+    L.memshare_status_string.argtypes = [I32]
+    L.memshare_status_string.restype = ctypes.c_char_p
+    L.memshare_abi_version.argtypes = []
+    L.memshare_abi_version.restype = I32
+    return L
+
+
+lib = _load()
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def status_string(code: int) -> str:
+    return lib.memshare_status_string(code).decode()
+
+
+def check(code: int, what: str = "memshare"):
+    if code != OK:
+        raise MemShareError(f"{what}: {status_string(code)}")
+    return code
+
+
+def abi_version() -> int:
+    return lib.memshare_abi_version()
+
+
+# ------------------------------------------------------------------------------------- a1
+def segment_steps_workspace_size(num_seqs: int) -> int:
+    return lib.memshare_segment_steps_workspace_size(num_seqs)
+
+
+def segment_steps(tokens, seq_tok_off, gen_start, seq_final, num_seqs, delim_ids, step_start, step_end, step_nbag,
+                  seq_step_off, step_cap, workspace, device_status, stream=None) -> int:
+    d = np.ascontiguousarray(delim_ids, np.int32)
+    return lib.memshare_segment_steps(_ptr(tokens), _ptr(seq_tok_off), _ptr(gen_start), _ptr(seq_final), num_seqs,
+                                      d.ctypes.data, d.size, _ptr(step_start), _ptr(step_end), _ptr(step_nbag),
+                                      _ptr(seq_step_off), step_cap, _ptr(workspace),
+                                      0 if workspace is None else workspace.numel() * workspace.element_size(),
+                                      _ptr(device_status), _stream(stream))
+
+
+# ----------------------------------------------------------------------------------- a2-a4
+def step_candidates_workspace_size(num_tokens, num_seqs, step_cap, match_cap) -> int:
+    return lib.memshare_step_candidates_workspace_size(num_tokens, num_seqs, step_cap, match_cap)
+
+
+def step_candidates(tokens, num_tokens, seq_tok_off, num_seqs, seq_step_off, step_start, step_end, step_nbag,
+                    step_cap, delim_ids, cur_mode, cur_begin, cur_end, block_table, table_stride, num_blocks,
+                    block_size, tau_s, top_k, pairing, matches, match_cap, num_matches, pairs, pair_cap, num_pairs,
+                    target_off, target_cap, num_targets, workspace, device_status, stream=None) -> int:
+    d = np.ascontiguousarray(delim_ids, np.int32)
+    return lib.memshare_step_candidates(
+        _ptr(tokens), num_tokens, _ptr(seq_tok_off), num_seqs, _ptr(seq_step_off), _ptr(step_start), _ptr(step_end),
+        _ptr(step_nbag), step_cap, d.ctypes.data, d.size, cur_mode, _ptr(cur_begin), _ptr(cur_end), _ptr(block_table),
+        table_stride, num_blocks, block_size, float(tau_s), top_k, pairing, _ptr(matches), match_cap,
+        _ptr(num_matches), _ptr(pairs), pair_cap, _ptr(num_pairs), _ptr(target_off), target_cap, _ptr(num_targets),
+        _ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
+        _ptr(device_status), _stream(stream))
+
+
+# ----------------------------------------------------------------------------------- a5-a6
+def block_distance_workspace_size(dims: Dims, pair_cap: int, target_cap: int) -> int:
+    return lib.memshare_block_distance_workspace_size(ctypes.byref(dims), pair_cap, target_cap)
+
+
+def block_distance(pool: KVPool | None, dims: Dims, pairs, target_off, num_pairs, num_targets, pair_cap, target_cap,
+                   mode, partial_sq, tau_b, distance, under, decisions, workspace, device_status, stream=None) -> int:
+    return lib.memshare_block_distance(
+        None if pool is None else ctypes.byref(pool), ctypes.byref(dims), _ptr(pairs), _ptr(target_off),
+        _ptr(num_pairs), _ptr(num_targets), pair_cap, target_cap, mode, _ptr(partial_sq), float(tau_b),
+        _ptr(distance), _ptr(under), _ptr(decisions), _ptr(workspace),
+        0 if workspace is None else workspace.numel() * workspace.element_size(), _ptr(device_status),
+        _stream(stream))
+
+
+# -------------------------------------------------------------------------------------- a7
+def remap_workspace_size(num_blocks: int, target_cap: int) -> int:
+    return lib.memshare_remap_workspace_size(num_blocks, target_cap)
+
+
+def remap(block_table, table_stride, num_seqs, refcount, num_blocks, free_list, free_count, decisions, num_targets,
+          target_cap, block_size, num_freed, affected_tokens, workspace, device_status, stream=None) -> int:
+    return lib.memshare_remap(_ptr(block_table), table_stride, num_seqs, _ptr(refcount), num_blocks, _ptr(free_list),
+                              _ptr(free_count), _ptr(decisions), _ptr(num_targets), target_cap, block_size,
+                              _ptr(num_freed), _ptr(affected_tokens), _ptr(workspace),
+                              0 if workspace is None else workspace.numel() * workspace.element_size(),
+                              _ptr(device_status), _stream(stream))

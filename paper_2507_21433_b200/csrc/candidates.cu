@@ -1,0 +1,627 @@
+// a2-a4 -- bag-of-words encoding, Stage-1 cosine filter and candidate block pairs.
+// PAPER.md:224-234 (Alg. 1 Stage 1), :254 (bag of words), :318 ('exceeding' -> strict >),
+// :267 / :319-320 (corresponding / pairwise blocks); readings R5-R14, R25.
+//
+// Design (B200): the bag of words of step k is never densified. The dot product with an
+// earlier step j is  <c_k, c_j> = sum over content tokens p of j of c_k[t_p],  so only the
+// CURRENT step needs a count table: an open-addressing hash table in shared memory (global
+// workspace for steps > 2048 content tokens), probed by one warp per history step while the
+// raw history tokens stream through L1/L2. Integer dot and norms are exact; the cosine is one
+// IEEE expression (__ddiv_rn / __dsqrt_rn / __dmul_rn), bit-identical to the C oracle.
+//
+// Three launches:
+//   encode  : one CTA per step: table -> n2 = sum count^2 (history norms)
+//   stage1  : one CTA per current step: table, warp-per-j dots, strict threshold, (cos desc,
+//             j asc) bitonic sort, top-K, stash survivors, count targets/pairs; the last CTA
+//             scans the per-step counts into output offsets
+//   fill    : one CTA per current step: write matches, targets, target_off, pairs
+#include <cfloat>
+#include <climits>
+
+#include "common.cuh"
+
+namespace ms {
+namespace {
+
+constexpr int kNT = 256;
+constexpr int kNW = kNT / 32;
+constexpr int kSmemSlots = 4096;       // smem hash table (steps with <= 2048 content tokens)
+constexpr int kCandCap = 1024;         // survivors held per current step
+constexpr int kChunk = kCandCap / 2;   // history steps per selection chunk
+constexpr int kMaxTgt = 4096;          // full blocks per step handled by the fill kernel
+constexpr int32_t kEmpty = -1;
+
+struct CandWs {
+  unsigned int* done;
+  unsigned long long* stash_alloc;
+  int32_t* step_seq;     // [step_cap]
+  int64_t* n2;           // [step_cap]
+  int32_t* cnt_m;        // [step_cap]
+  int32_t* cnt_t;
+  int32_t* cnt_p;
+  int64_t* stash_base;   // [step_cap]
+  int64_t* off_m;        // [step_cap+1]
+  int64_t* off_t;
+  int64_t* off_p;
+  double* stash_cos;     // [match_cap]
+  int32_t* stash_j;
+  int32_t* gkeys;        // [4*num_tokens]
+  int32_t* gcnts;
+};
+
+CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_cap) {
+  CandWs c;
+  c.done = w.take<unsigned int>(1);
+  c.stash_alloc = w.take<unsigned long long>(1);
+  c.step_seq = w.take<int32_t>(step_cap + 1);
+  c.n2 = w.take<int64_t>(step_cap + 1);
+  c.cnt_m = w.take<int32_t>(step_cap + 1);
+  c.cnt_t = w.take<int32_t>(step_cap + 1);
+  c.cnt_p = w.take<int32_t>(step_cap + 1);
+  c.stash_base = w.take<int64_t>(step_cap + 1);
+  c.off_m = w.take<int64_t>(step_cap + 1);
+  c.off_t = w.take<int64_t>(step_cap + 1);
+  c.off_p = w.take<int64_t>(step_cap + 1);
+  c.stash_cos = w.take<double>(match_cap + 1);
+  c.stash_j = w.take<int32_t>(match_cap + 1);
+  c.gkeys = w.take<int32_t>(4 * num_tokens + 1);
+  c.gcnts = w.take<int32_t>(4 * num_tokens + 1);
+  return c;
+}
+
+struct CandArgs {
+  const int32_t* tokens;
+  const int64_t* seq_tok_off;
+  int32_t num_seqs;
+  const int64_t* seq_step_off;
+  const int32_t* step_start;
+  const int32_t* step_end;
+  const int32_t* step_nbag;
+  int64_t step_cap;
+  Delims dl;
+  int32_t cur_mode;
+  const int32_t* cur_begin;
+  const int32_t* cur_end;
+  const int32_t* table;
+  int32_t table_stride;
+  int32_t num_blocks;
+  int32_t block_size;
+  double tau_s;
+  int32_t top_k;
+  int32_t pairing;
+  memshare_step_match* matches;
+  int64_t match_cap;
+  int64_t* num_matches;
+  memshare_block_pair* pairs;
+  int64_t pair_cap;
+  int64_t* num_pairs;
+  int64_t* target_off;
+  int64_t target_cap;
+  int64_t* num_targets;
+  int32_t* status;
+  CandWs ws;
+};
+
+__device__ __forceinline__ int64_t total_steps(const CandArgs& a) {
+  const int64_t g = __ldcg(a.seq_step_off + a.num_seqs);
+  return g < a.step_cap ? g : a.step_cap;
+}
+
+__device__ __forceinline__ uint32_t hash_slot(int32_t tok, uint32_t mask) {
+  return ((uint32_t)tok * 0x9E3779B1u) & mask;
+}
+
+__device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) { return x <= 1 ? 1u : 1u << (32 - __clz(x - 1)); }
+__device__ __forceinline__ uint32_t pow2_floor(uint32_t x) { return 1u << (31 - __clz(x)); }
+
+// Count table of one step: keys/cnts live in smem (small steps) or in the step's private
+// region of the global workspace (4 slots per token of the step).
+struct Table {
+  int32_t* keys;
+  int32_t* cnts;
+  uint32_t mask;
+  bool global;
+};
+
+__device__ Table build_table(const CandArgs& a, int32_t* s_keys, int32_t* s_cnts, const int32_t* t, int64_t tok_base,
+                             int32_t start, int32_t end, int32_t nbag) {
+  Table tb;
+  uint32_t cap;
+  if (nbag <= kSmemSlots / 2) {
+    cap = pow2_ceil(2u * (uint32_t)(nbag > 32 ? nbag : 32));
+    tb.keys = s_keys;
+    tb.cnts = s_cnts;
+    tb.global = false;
+  } else {
+    cap = pow2_floor(4u * (uint32_t)(end - start));
+    tb.keys = a.ws.gkeys + 4 * (tok_base + start);
+    tb.cnts = a.ws.gcnts + 4 * (tok_base + start);
+    tb.global = true;
+  }
+  tb.mask = cap - 1;
+  for (uint32_t i = threadIdx.x; i < cap; i += kNT) {
+    tb.keys[i] = kEmpty;
+    tb.cnts[i] = 0;
+  }
+  __syncthreads();
+  for (int32_t p = start + threadIdx.x; p < end; p += kNT) {
+    const int32_t tok = t[p];
+    if (is_delim(tok, a.dl)) continue;
+    uint32_t slot = hash_slot(tok, tb.mask);
+    for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
+      const int32_t prev = atomicCAS(tb.keys + slot, kEmpty, tok);
+      if (prev == kEmpty || prev == tok) {
+        atomicAdd(tb.cnts + slot, 1);
+        break;
+      }
+      slot = (slot + 1) & tb.mask;
+    }
+  }
+  __syncthreads();
+  return tb;
+}
+
+__device__ __forceinline__ int32_t table_get(const Table& tb, int32_t tok) {
+  uint32_t slot = hash_slot(tok, tb.mask);
+  for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
+    const int32_t k = tb.global ? __ldcg(tb.keys + slot) : tb.keys[slot];
+    if (k == tok) return tb.global ? __ldcg(tb.cnts + slot) : tb.cnts[slot];
+    if (k == kEmpty) return 0;
+    slot = (slot + 1) & tb.mask;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {
+  int32_t lo = 0, hi = a.num_seqs - 1;   // last s with seq_step_off[s] <= g
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(a.seq_step_off + mid) <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
+  __shared__ int32_t s_keys[kSmemSlots];
+  __shared__ int32_t s_cnts[kSmemSlots];
+  __shared__ int64_t sh[kNW + 1];
+  const int64_t G = total_steps(a);
+  for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+    const int32_t s = seq_of_step(a, g);
+    const int64_t tok_base = a.seq_tok_off[s];
+    const int32_t nbag = a.step_nbag[g];
+    int64_t n2 = 0;
+    if (nbag > 0) {
+      const Table tb = build_table(a, s_keys, s_cnts, a.tokens + tok_base, tok_base, a.step_start[g], a.step_end[g], nbag);
+      for (uint32_t i = threadIdx.x; i <= tb.mask; i += kNT) {
+        const int64_t c = tb.global ? __ldcg(tb.cnts + i) : tb.cnts[i];
+        n2 += c * c;
+      }
+    }
+    n2 = block_sum<kNT>(n2, sh);
+    if (threadIdx.x == 0) {
+      a.ws.n2[g] = n2;
+      a.ws.step_seq[g] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------------------------------------
+// candidate list helpers
+__device__ __forceinline__ bool cand_before(double ca, int32_t ja, double cb, int32_t jb) {
+  return ca > cb || (ca == cb && ja < jb);
+}
+
+// bitonic sort of (cos desc, j asc) over n entries padded to a power of two
+__device__ void sort_cands(double* cs, int32_t* js, int n) {
+  if (n <= 1) return;
+  const int np = (int)pow2_ceil((uint32_t)n);
+  for (int i = n + threadIdx.x; i < np; i += kNT) {
+    cs[i] = -2.0;
+    js[i] = INT_MAX;
+  }
+  __syncthreads();
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < np; i += kNT) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const bool swap = up ? cand_before(cs[ixj], js[ixj], cs[i], js[i]) : cand_before(cs[i], js[i], cs[ixj], js[ixj]);
+          if (swap) {
+            const double tc = cs[i]; cs[i] = cs[ixj]; cs[ixj] = tc;
+            const int32_t tj = js[i]; js[i] = js[ixj]; js[ixj] = tj;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ void sort_ints(int32_t* v, int n) {
+  if (n <= 1) return;
+  const int np = (int)pow2_ceil((uint32_t)n);
+  for (int i = n + threadIdx.x; i < np; i += kNT) v[i] = INT_MAX;
+  __syncthreads();
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < np; i += kNT) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          if (up ? v[ixj] < v[i] : v[i] < v[ixj]) {
+            const int32_t t = v[i]; v[i] = v[ixj]; v[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Candidate steps of one current step in ascending j, with their full-block ranges.
+struct Cands {
+  int m;
+  int32_t* jasc;
+  int32_t* flo;
+  int32_t* flen;
+  int32_t* cum;    // CROSS prefix of flen [m+1]
+};
+
+__device__ __forceinline__ int32_t ceil_div(int32_t a, int32_t b) { return (a + b - 1) / b; }
+
+__device__ void prepare_cands(const CandArgs& a, Cands& c, int64_t gfirst) {
+  sort_ints(c.jasc, c.m);
+  for (int r = threadIdx.x; r < c.m; r += kNT) {
+    const int64_t gj = gfirst + c.jasc[r];
+    const int32_t lo = ceil_div(a.step_start[gj], a.block_size), hi = a.step_end[gj] / a.block_size;
+    c.flo[r] = lo;
+    c.flen[r] = hi > lo ? hi - lo : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int r = 0; r < c.m; ++r) { c.cum[r] = acc; acc += c.flen[r]; }
+    c.cum[c.m] = acc;
+  }
+  __syncthreads();
+}
+
+// Logical source block of slot e for target offset i (-1 = no block in this slot).
+__device__ __forceinline__ int32_t slot_logical(const Cands& c, int pairing, int32_t i, int32_t e) {
+  if (pairing == MEMSHARE_PAIR_ALIGNED) return i < c.flen[e] ? c.flo[e] + i : -1;
+  int lo = 0, hi = c.m - 1;   // last r with cum[r] <= e
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (c.cum[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return c.flo[lo] + (e - c.cum[lo]);
+}
+
+__device__ __forceinline__ int32_t phys_of(const CandArgs& a, const int32_t* trow, int32_t lg) {
+  if (lg < 0 || lg >= a.table_stride) { set_status(a.status, MEMSHARE_ERR_CORRUPTION); return INT_MIN; }
+  const int32_t p = trow[lg];
+  if (p < 0 || p >= a.num_blocks) set_status(a.status, MEMSHARE_ERR_CORRUPTION);
+  return p;
+}
+
+// Warp-cooperative: kept (deduplicated) sources of target offset i. If `out` is non-null the
+// kept pairs are written from out[0]. Returns the kept count (all lanes).
+__device__ int32_t target_sources(const CandArgs& a, const Cands& c, const int32_t* trow, int32_t s, int32_t i,
+                                  int32_t tl, int32_t tphys, int32_t tidx, memshare_block_pair* out, int64_t out_pos,
+                                  int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int32_t nslots = a.pairing == MEMSHARE_PAIR_ALIGNED ? c.m : c.cum[c.m];
+  int32_t kept_total = 0;
+  for (int32_t eb = 0; eb < nslots; eb += 32) {
+    const int32_t e = eb + lane;
+    int32_t lg = e < nslots ? slot_logical(c, a.pairing, i, e) : -1;
+    bool keep = lg >= 0;
+    int32_t ph = keep ? phys_of(a, trow, lg) : -1;
+    if (keep) {
+      for (int32_t e2 = 0; e2 < e; ++e2) {
+        const int32_t lg2 = slot_logical(c, a.pairing, i, e2);
+        if (lg2 >= 0 && lg2 < a.table_stride && trow[lg2] == ph) { keep = false; break; }
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (out != nullptr && keep) {
+      const int64_t pos = out_pos + kept_total + __popc(bal & ((1u << lane) - 1u));
+      if (pos < cap) {
+        memshare_block_pair pr;
+        pr.seq = s; pr.target_idx = tidx; pr.target_logical = tl; pr.source_logical = lg;
+        pr.target_phys = tphys; pr.source_phys = ph;
+        out[pos] = pr;
+      }
+    }
+    kept_total += __popc(bal);
+  }
+  return kept_total;
+}
+
+__device__ __forceinline__ bool is_current(const CandArgs& a, int32_t s, int64_t k, int64_t S) {
+  if (a.cur_mode == MEMSHARE_CUR_ALL) return true;
+  if (a.cur_mode == MEMSHARE_CUR_LAST) return k == S - 1;
+  return k >= a.cur_begin[s] && k < a.cur_end[s];
+}
+
+struct SelSmem {
+  int32_t keys[kSmemSlots];
+  int32_t cnts[kSmemSlots];
+  double cs[kCandCap];
+  int32_t js[kCandCap];
+  int32_t jasc[kCandCap];
+  int32_t flo[kCandCap];
+  int32_t flen[kCandCap];
+  int32_t cum[kCandCap + 1];
+  int64_t sh[kNW + 1];
+  int count;
+  int overflow;
+  int64_t acc_t;
+  int64_t acc_p;
+};
+
+__global__ void __launch_bounds__(kNT) stage1_kernel(CandArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t G = total_steps(a);
+  for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+    const int32_t s = a.ws.step_seq[g];
+    const int64_t gfirst = a.seq_step_off[s];
+    const int64_t S = a.seq_step_off[s + 1] - gfirst;
+    const int64_t k = g - gfirst;
+    const int32_t nbag = a.step_nbag[g];
+    if (nbag == 0 || !is_current(a, s, k, S)) {
+      if (threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
+      continue;
+    }
+    const int64_t tok_base = a.seq_tok_off[s];
+    const int32_t* t = a.tokens + tok_base;
+    const Table tb = build_table(a, sm.keys, sm.cnts, t, tok_base, a.step_start[g], a.step_end[g], nbag);
+    const double n2k = (double)a.ws.n2[g];
+    if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
+    __syncthreads();
+    const bool compact = a.top_k > 0 && a.top_k <= kCandCap / 2;
+    for (int64_t jb = 0; jb < k; jb += kChunk) {
+      const int64_t je = (jb + kChunk < k) ? jb + kChunk : k;
+      for (int64_t j = jb + w; j < je; j += kNW) {
+        const int64_t gj = gfirst + j;
+        if (a.step_nbag[gj] == 0) continue;              // void history step (reading R5)
+        int64_t dot = 0;
+        const int32_t e = a.step_end[gj];
+        for (int32_t p = a.step_start[gj] + lane; p < e; p += 32) {
+          const int32_t tok = t[p];
+          if (!is_delim(tok, a.dl)) dot += table_get(tb, tok);
+        }
+        dot = warp_sum(dot);
+        if (lane == 0) {
+          // sim = <v_curr, v_i> / (||v_curr|| ||v_i||), reading R12
+          const double cs = __ddiv_rn(__ll2double_rn(dot), __dsqrt_rn(__dmul_rn(n2k, __ll2double_rn(a.ws.n2[gj]))));
+          if (cs > a.tau_s) {                             // strict: "exceeding"
+            const int idx = atomicAdd(&sm.count, 1);
+            if (idx < kCandCap) { sm.cs[idx] = cs; sm.js[idx] = (int32_t)j; }
+            else sm.overflow = 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (compact && sm.count > kCandCap / 2) {
+        sort_cands(sm.cs, sm.js, sm.count);
+        __syncthreads();
+        if (threadIdx.x == 0) sm.count = a.top_k;
+        __syncthreads();
+      }
+    }
+    if (sm.overflow) {
+      if (threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+      __syncthreads();
+    }
+    int m = sm.count < kCandCap ? sm.count : kCandCap;
+    sort_cands(sm.cs, sm.js, m);
+    if (a.top_k > 0 && m > a.top_k) m = a.top_k;
+    // stash the ranked survivors for the fill kernel
+    __shared__ unsigned long long s_base;
+    if (threadIdx.x == 0) {
+      s_base = m > 0 ? atomicAdd(a.ws.stash_alloc, (unsigned long long)m) : 0ull;
+      if ((int64_t)(s_base + m) > a.match_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+    }
+    __syncthreads();
+    const int64_t base = (int64_t)s_base;
+    for (int r = threadIdx.x; r < m; r += kNT) {
+      if (base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
+      sm.jasc[r] = sm.js[r];
+    }
+    if (threadIdx.x == 0) { sm.acc_t = 0; sm.acc_p = 0; }
+    __syncthreads();
+    // a4: count targets and deduplicated pairs of this step
+    Cands c{m, sm.jasc, sm.flo, sm.flen, sm.cum};
+    prepare_cands(a, c, gfirst);
+    const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
+    const int32_t nt = (m > 0 && fk_hi > fk_lo) ? fk_hi - fk_lo : 0;
+    if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+    const int32_t* trow = a.table + (int64_t)s * a.table_stride;
+    int64_t my_t = 0, my_p = 0;
+    for (int32_t i = w; i < nt; i += kNW) {
+      const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
+      my_t += kept > 0 ? 1 : 0;
+      my_p += kept;
+    }
+    if (lane == 0) { atomicAdd((unsigned long long*)&sm.acc_t, (unsigned long long)my_t); atomicAdd((unsigned long long*)&sm.acc_p, (unsigned long long)my_p); }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.ws.cnt_m[g] = m;
+      a.ws.cnt_t[g] = (int32_t)sm.acc_t;
+      a.ws.cnt_p[g] = (int32_t)sm.acc_p;
+      a.ws.stash_base[g] = base;
+    }
+    __syncthreads();
+  }
+  if (last_block_done(a.ws.done)) {
+    cta_scan_counts<kNT>(a.ws.cnt_m, a.ws.off_m, G, sm.sh);
+    cta_scan_counts<kNT>(a.ws.cnt_t, a.ws.off_t, G, sm.sh);
+    cta_scan_counts<kNT>(a.ws.cnt_p, a.ws.off_p, G, sm.sh);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t M = a.ws.off_m[G], T = a.ws.off_t[G], P = a.ws.off_p[G];
+      *a.num_matches = M;
+      *a.num_targets = T;
+      *a.num_pairs = P;
+      if (M > a.match_cap || T > a.target_cap || P > a.pair_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+      if (T <= a.target_cap) a.target_off[T] = P;
+    }
+  }
+}
+
+struct FillSmem {
+  double cs[kCandCap];
+  int32_t js[kCandCap];
+  int32_t jasc[kCandCap];
+  int32_t flo[kCandCap];
+  int32_t flen[kCandCap];
+  int32_t cum[kCandCap + 1];
+  int32_t tc[kMaxTgt];
+  int64_t tpos[kMaxTgt];   // pair offset (within the step) of each target offset i
+  int32_t tnum[kMaxTgt];   // target number (within the step), -1 if no pair
+  int64_t sh[kNW + 1];
+};
+
+__global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FillSmem& sm = *reinterpret_cast<FillSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t G = total_steps(a);
+  for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+    const int m = a.ws.cnt_m[g];
+    if (m == 0) continue;
+    const int32_t s = a.ws.step_seq[g];
+    const int64_t gfirst = a.seq_step_off[s];
+    const int64_t k = g - gfirst;
+    const int64_t sbase = a.ws.stash_base[g];
+    if (sbase + m > a.match_cap) continue;              // stash overflowed: CAPACITY already set
+    const int64_t mo = a.ws.off_m[g];
+    for (int r = threadIdx.x; r < m; r += kNT) {
+      const double cs = a.ws.stash_cos[sbase + r];
+      const int32_t j = a.ws.stash_j[sbase + r];
+      sm.jasc[r] = j;
+      if (mo + r < a.match_cap) {
+        memshare_step_match mt;
+        mt.seq = s; mt.step = (int32_t)k; mt.cand_step = j; mt.rank = r; mt.cosine = cs;
+        a.matches[mo + r] = mt;
+      }
+    }
+    __syncthreads();
+    Cands c{m, sm.jasc, sm.flo, sm.flen, sm.cum};
+    prepare_cands(a, c, gfirst);
+    const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
+    int32_t nt = fk_hi > fk_lo ? fk_hi - fk_lo : 0;
+    if (nt > kMaxTgt) continue;                          // CAPACITY already set by stage1
+    const int32_t* trow = a.table + (int64_t)s * a.table_stride;
+    for (int32_t i = w; i < nt; i += kNW) {
+      const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
+      if (lane == 0) sm.tc[i] = kept;
+    }
+    __syncthreads();
+    // per-target pair offsets and target numbers within the step (block scans)
+    int64_t pcarry = 0, tcarry = 0;
+    for (int32_t ib = 0; ib < nt; ib += kNT) {
+      const int32_t i = ib + threadIdx.x;
+      const int64_t v = i < nt ? sm.tc[i] : 0;
+      int64_t tot;
+      const int64_t ex = block_excl_scan<kNT>(v, tot, sm.sh);
+      int64_t tt;
+      const int64_t tex = block_excl_scan<kNT>(v > 0 ? 1 : 0, tt, sm.sh);
+      if (i < nt) { sm.tpos[i] = pcarry + ex; sm.tnum[i] = v > 0 ? (int32_t)(tcarry + tex) : -1; }
+      pcarry += tot;
+      tcarry += tt;
+    }
+    __syncthreads();
+    const int64_t po = a.ws.off_p[g], to = a.ws.off_t[g];
+    for (int32_t i = w; i < nt; i += kNW) {
+      if (sm.tnum[i] < 0) continue;
+      const int64_t tidx = to + sm.tnum[i];
+      const int32_t tl = fk_lo + i;
+      const int32_t tphys = phys_of(a, trow, tl);
+      target_sources(a, c, trow, s, i, tl, tphys, (int32_t)tidx, a.pairs, po + sm.tpos[i], a.pair_cap);
+      if (lane == 0 && tidx < a.target_cap) a.target_off[tidx] = po + sm.tpos[i];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace ms
+
+using namespace ms;
+
+extern "C" size_t memshare_step_candidates_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap,
+                                                          int64_t match_cap) {
+  if (num_tokens < 0 || num_seqs < 0 || step_cap < 0 || match_cap < 0) return 0;
+  Ws w{nullptr, 0};
+  cand_layout(w, num_tokens, step_cap, match_cap);
+  return w.size();
+}
+
+extern "C" memshare_status memshare_step_candidates(
+    const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off, int32_t num_seqs,
+    const int64_t* seq_step_off, const int32_t* step_start, const int32_t* step_end, const int32_t* step_nbag,
+    int64_t step_cap, const int32_t* delim_ids_host, int32_t num_delims, int32_t cur_mode, const int32_t* cur_begin,
+    const int32_t* cur_end, const int32_t* block_table, int32_t table_stride, int32_t num_blocks, int32_t block_size,
+    double tau_s, int32_t top_k, int32_t pairing, memshare_step_match* matches, int64_t match_cap,
+    int64_t* num_matches, memshare_block_pair* pairs, int64_t pair_cap, int64_t* num_pairs, int64_t* target_off,
+    int64_t target_cap, int64_t* num_targets, void* workspace, size_t workspace_bytes, int32_t* device_status,
+    void* stream) {
+  if (num_tokens < 0 || num_seqs < 0 || step_cap < 0 || match_cap < 0 || pair_cap < 0 || target_cap < 0)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (num_delims < 1 || num_delims > MEMSHARE_MAX_DELIMS || !delim_ids_host) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (cur_mode < MEMSHARE_CUR_ALL || cur_mode > MEMSHARE_CUR_RANGE) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (cur_mode == MEMSHARE_CUR_RANGE && num_seqs > 0 && (!cur_begin || !cur_end)) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (pairing != MEMSHARE_PAIR_ALIGNED && pairing != MEMSHARE_PAIR_CROSS) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (!(tau_s >= -1.0 && tau_s <= 1.0) || top_k < 0 || block_size < 1 || table_stride < 0 || num_blocks < 0)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (num_tokens > (int64_t)INT32_MAX / 4) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (!seq_tok_off || !seq_step_off || !num_matches || !num_pairs || !num_targets || !target_off || !workspace ||
+      !device_status)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (num_seqs > 0 && (!tokens || !block_table)) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (step_cap > 0 && (!step_start || !step_end || !step_nbag)) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if ((match_cap > 0 && !matches) || (pair_cap > 0 && !pairs)) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < memshare_step_candidates_workspace_size(num_tokens, num_seqs, step_cap, match_cap))
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+
+  CandArgs a{};
+  a.tokens = tokens; a.seq_tok_off = seq_tok_off; a.num_seqs = num_seqs; a.seq_step_off = seq_step_off;
+  a.step_start = step_start; a.step_end = step_end; a.step_nbag = step_nbag; a.step_cap = step_cap;
+  a.dl.n = num_delims;
+  for (int i = 0; i < num_delims; ++i) a.dl.id[i] = delim_ids_host[i];
+  a.cur_mode = cur_mode; a.cur_begin = cur_begin; a.cur_end = cur_end;
+  a.table = block_table; a.table_stride = table_stride; a.num_blocks = num_blocks; a.block_size = block_size;
+  a.tau_s = tau_s; a.top_k = top_k; a.pairing = pairing;
+  a.matches = matches; a.match_cap = match_cap; a.num_matches = num_matches;
+  a.pairs = pairs; a.pair_cap = pair_cap; a.num_pairs = num_pairs;
+  a.target_off = target_off; a.target_cap = target_cap; a.num_targets = num_targets;
+  a.status = device_status;
+  Ws w{static_cast<char*>(workspace), 0};
+  a.ws = cand_layout(w, num_tokens, step_cap, match_cap);
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem));
+    cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FillSmem));
+    attr_set = true;
+  }
+  // done counter + stash allocator (adjacent, first two allocations)
+  if (cudaMemsetAsync(a.ws.done, 0, 256, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  if (cudaMemsetAsync(a.ws.stash_alloc, 0, sizeof(unsigned long long), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  const int sms = sm_count();
+  const int64_t gcap = step_cap < 1 ? 1 : step_cap;
+  const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
+  const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
+  encode_kernel<<<grid_enc, kNT, 0, st>>>(a);
+  stage1_kernel<<<grid_sel, kNT, sizeof(SelSmem), st>>>(a);
+  fill_kernel<<<grid_sel, kNT, sizeof(FillSmem), st>>>(a);
+  return launch_status();
+}

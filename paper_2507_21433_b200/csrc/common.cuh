@@ -1,0 +1,137 @@
+// Shared device helpers of the CUDA path (sm_100a). Nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "memshare.h"
+
+namespace ms {
+
+constexpr int kWarp = 32;
+
+struct Delims {
+  int32_t n;
+  int32_t id[MEMSHARE_MAX_DELIMS];
+};
+
+__device__ __forceinline__ bool is_delim(int32_t t, const Delims& d) {
+  bool r = false;
+#pragma unroll
+  for (int i = 0; i < MEMSHARE_MAX_DELIMS; ++i) r |= (i < d.n) && (t == d.id[i]);
+  return r;
+}
+
+// Sticky first-error device status (first writer wins).
+__device__ __forceinline__ void set_status(int32_t* st, int32_t code) {
+  if (st != nullptr) atomicCAS(st, 0, code);
+}
+
+// Bump allocator over the caller's workspace; the same sequence of take() calls in
+// "measure" mode (base == nullptr) gives the required size.
+struct Ws {
+  char* base;
+  size_t off;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+  size_t size() const { return (off + 255) & ~size_t(255); }
+};
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan of int64; `sh` must hold >= NT/32 + 1 entries. Returns the
+// exclusive prefix of this thread, writes the block total to `total`.
+template <int NT>
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t& total, int64_t* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t s = lane < NT / 32 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) sh[lane] = s;   // inclusive warp totals
+  }
+  __syncthreads();
+  const int64_t warp_prefix = w > 0 ? sh[w - 1] : 0;
+  total = sh[NT / 32 - 1];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+template <int NT>
+__device__ __forceinline__ int64_t block_sum(int64_t v, int64_t* sh) {
+  int64_t t;
+  block_excl_scan<NT>(v, t, sh);
+  return t;
+}
+
+// "Last CTA done" election for fused count -> scan kernels. All threads call it.
+__device__ __forceinline__ bool last_block_done(unsigned int* ctr) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(ctr, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// Exclusive scan of a device array of `n` int32 counts into int64 offsets by ONE CTA.
+// out_off[n] receives the total. Reads bypass L1 (values written by other CTAs).
+template <int NT>
+__device__ void cta_scan_counts(const int32_t* cnt, int64_t* out_off, int64_t n, int64_t* sh) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += NT) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < n ? (int64_t)__ldcg(cnt + i) : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan<NT>(v, tot, sh);
+    if (i < n) out_off[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) out_off[n] = carry;
+}
+
+inline int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline memshare_status launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MEMSHARE_OK : MEMSHARE_ERR_CUDA;
+}
+
+}  // namespace ms

@@ -1,0 +1,179 @@
+"""Device-buffer plumbing around the four C-ABI calls (no arithmetic of the method here).
+
+``MemSharePath`` owns the torch CUDA buffers of one pool (trace, block table, refcounts, free
+list, KV pool, outputs, workspaces) and enqueues the calls in path order on one stream:
+
+    segment_steps -> step_candidates -> block_distance -> remap        (one round)
+
+Counts stay on the device between calls; ``read_*`` methods synchronise and copy to host for
+tests and reporting only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+@dataclass
+class Caps:
+    step: int
+    match: int
+    pair: int
+    target: int
+
+
+def _dev_i32(a, dev):
+    return torch.as_tensor(np.ascontiguousarray(a, np.int32), device=dev)
+
+
+def _dev_i64(a, dev):
+    return torch.as_tensor(np.ascontiguousarray(a, np.int64), device=dev)
+
+
+class MemSharePath:
+    def __init__(self, tokens, seq_tok_off, gen_start, final, delim_ids, table, refcount, free_list, free_count,
+                 k_pool, v_pool, layer_stride, block_stride, num_blocks, num_layers, h_local, h_global, head_dim,
+                 block_size, caps: Caps | None = None, device="cuda", stream=None):
+        self.dev = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self.delims = np.ascontiguousarray(delim_ids, np.int32)
+        self.num_seqs = int(len(gen_start))
+        self.num_tokens = int(len(tokens))
+        self.tokens = _dev_i32(tokens, self.dev)
+        self.seq_tok_off = _dev_i64(seq_tok_off, self.dev)
+        self.gen_start = _dev_i32(gen_start, self.dev)
+        self.final = torch.as_tensor(np.ascontiguousarray(final, np.uint8), device=self.dev)
+        table = np.ascontiguousarray(table, np.int32)
+        self.table_stride = int(table.shape[1])
+        self.table = _dev_i32(table, self.dev)
+        self.refcount = _dev_i32(refcount, self.dev)
+        self.free_list = _dev_i32(free_list, self.dev)
+        self.free_count = torch.tensor([int(free_count)], dtype=torch.int64, device=self.dev)
+        self.num_blocks = int(num_blocks)
+        self.k_pool, self.v_pool = k_pool, v_pool
+        self.pool = L.KVPool(k_pool.data_ptr() if k_pool is not None else None,
+                             v_pool.data_ptr() if v_pool is not None else None, layer_stride, block_stride,
+                             num_blocks, 0)
+        self.dims = L.Dims(num_layers, h_local, h_global, head_dim, block_size)
+        self.block_size = block_size
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        z64 = lambda: torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.num_matches, self.num_pairs, self.num_targets = z64(), z64(), z64()
+        self.num_freed, self.affected = z64(), z64()
+        self.seq_step_off = torch.zeros(self.num_seqs + 1, dtype=torch.int64, device=self.dev)
+        self.partial_sq = None
+        self.set_caps(caps or Caps(step=max(1, self.num_tokens), match=max(1024, self.num_tokens),
+                                   pair=max(4096, self.num_tokens), target=max(2048, self.num_tokens // block_size + 1)))
+
+    # ------------------------------------------------------------------ buffers
+    def set_caps(self, caps: Caps):
+        self.caps = caps
+        d = self.dev
+        e = lambda n, dt: torch.empty(max(1, n), dtype=dt, device=d)
+        self.step_start, self.step_end, self.step_nbag = (e(caps.step, torch.int32) for _ in range(3))
+        self.matches = e(caps.match * 24, torch.uint8)
+        self.pairs = e(caps.pair * 24, torch.uint8)
+        self.target_off = e(caps.target + 1, torch.int64)
+        self.distance = e(caps.pair, torch.float32)
+        self.under = e(caps.pair, torch.uint8)
+        self.decisions = e(caps.target * 32, torch.uint8)
+        ws = max(L.segment_steps_workspace_size(self.num_seqs),
+                 L.step_candidates_workspace_size(self.num_tokens, self.num_seqs, caps.step, caps.match),
+                 L.block_distance_workspace_size(self.dims, caps.pair, caps.target),
+                 L.remap_workspace_size(self.num_blocks, caps.target))
+        self.workspace = e(ws, torch.uint8)
+
+    def alloc_partial(self):
+        self.partial_sq = torch.zeros(max(1, self.caps.pair) * self.dims.num_layers * 2, dtype=torch.float32,
+                                      device=self.dev)
+        return self.partial_sq
+
+    # ------------------------------------------------------------------ the four calls
+    def segment(self):
+        L.check(L.segment_steps(self.tokens, self.seq_tok_off, self.gen_start, self.final, self.num_seqs, self.delims,
+                                self.step_start, self.step_end, self.step_nbag, self.seq_step_off, self.caps.step,
+                                self.workspace, self.status, self.stream), "segment_steps")
+
+    def candidates(self, tau_s, top_k=0, pairing=L.PAIR_ALIGNED, cur_mode=L.CUR_ALL, cur_begin=None, cur_end=None):
+        cb = None if cur_begin is None else _dev_i32(cur_begin, self.dev)
+        ce = None if cur_end is None else _dev_i32(cur_end, self.dev)
+        self._cur_keep = (cb, ce)
+        L.check(L.step_candidates(self.tokens, self.num_tokens, self.seq_tok_off, self.num_seqs, self.seq_step_off,
+                                  self.step_start, self.step_end, self.step_nbag, self.caps.step, self.delims, cur_mode,
+                                  cb, ce, self.table, self.table_stride, self.num_blocks, self.block_size, tau_s, top_k,
+                                  pairing, self.matches, self.caps.match, self.num_matches, self.pairs, self.caps.pair,
+                                  self.num_pairs, self.target_off, self.caps.target, self.num_targets, self.workspace,
+                                  self.status, self.stream), "step_candidates")
+
+    def distance_call(self, tau_b, mode=L.DIST_FULL, partial_sq=None):
+        ps = partial_sq if partial_sq is not None else self.partial_sq
+        L.check(L.block_distance(None if mode == L.DIST_FINALIZE else self.pool, self.dims, self.pairs,
+                                 self.target_off, self.num_pairs, self.num_targets, self.caps.pair, self.caps.target,
+                                 mode, ps, tau_b, self.distance, self.under, self.decisions, self.workspace,
+                                 self.status, self.stream), "block_distance")
+
+    def remap(self):
+        L.check(L.remap(self.table, self.table_stride, self.num_seqs, self.refcount, self.num_blocks, self.free_list,
+                        self.free_count, self.decisions, self.num_targets, self.caps.target, self.block_size,
+                        self.num_freed, self.affected, self.workspace, self.status, self.stream), "remap")
+
+    def round(self, tau_s, tau_b, top_k=0, pairing=L.PAIR_ALIGNED, cur_mode=L.CUR_ALL, cur_begin=None, cur_end=None):
+        self.segment()
+        self.candidates(tau_s, top_k, pairing, cur_mode, cur_begin, cur_end)
+        self.distance_call(tau_b)
+        self.remap()
+
+    # ------------------------------------------------------------------ host reads (sync)
+    def read_status(self) -> int:
+        return int(self.status.item())
+
+    def counts(self):
+        torch.cuda.synchronize(self.dev)
+        return {"steps": int(self.seq_step_off[-1].item()), "matches": int(self.num_matches.item()),
+                "pairs": int(self.num_pairs.item()), "targets": int(self.num_targets.item())}
+
+    def autosize(self, tau_s, top_k=0, pairing=L.PAIR_ALIGNED, cur_mode=L.CUR_ALL, cur_begin=None, cur_end=None,
+                 slack=1.0):
+        """Count-then-fill: run a1-a4, read the device counts and size every buffer to fit."""
+        self.segment()
+        self.candidates(tau_s, top_k, pairing, cur_mode, cur_begin, cur_end)
+        c = self.counts()
+        self.status.zero_()
+        caps = Caps(step=self.caps.step, match=max(1, int(c["matches"] * slack)),
+                    pair=max(1, int(c["pairs"] * slack)), target=max(1, int(c["targets"] * slack)))
+        self.set_caps(caps)
+        return c
+
+    def read_steps(self):
+        torch.cuda.synchronize(self.dev)
+        n = min(int(self.seq_step_off[-1].item()), self.caps.step)
+        return {"step_start": self.step_start[:n].cpu().numpy(), "step_end": self.step_end[:n].cpu().numpy(),
+                "step_nbag": self.step_nbag[:n].cpu().numpy(), "seq_step_off": self.seq_step_off.cpu().numpy()}
+
+    def read_candidates(self):
+        c = self.counts()
+        M, P, T = (min(c[k], cap) for k, cap in (("matches", self.caps.match), ("pairs", self.caps.pair),
+                                                  ("targets", self.caps.target)))
+        m = self.matches[:M * 24].cpu().numpy().view(L.MATCH_DTYPE)
+        p = self.pairs[:P * 24].cpu().numpy().view(L.PAIR_DTYPE)
+        toff = self.target_off[:T + 1].cpu().numpy()
+        return {"matches": {k: m[k].copy() for k in L.MATCH_DTYPE.names},
+                "pairs": {k: p[k].copy() for k in L.PAIR_DTYPE.names}, "target_off": toff}
+
+    def read_distance(self):
+        c = self.counts()
+        P, T = min(c["pairs"], self.caps.pair), min(c["targets"], self.caps.target)
+        dec = self.decisions[:T * 32].cpu().numpy().view(L.DECISION_DTYPE)
+        return {"distance": self.distance[:P].cpu().numpy(), "under": self.under[:P].cpu().numpy(),
+                "decisions": {k: dec[k].copy() for k in L.DECISION_DTYPE.names}}
+
+    def read_state(self):
+        torch.cuda.synchronize(self.dev)
+        return {"table": self.table.view(self.num_seqs, self.table_stride).cpu().numpy(),
+                "refcount": self.refcount.cpu().numpy(), "free_list": self.free_list.cpu().numpy(),
+                "free_count": int(self.free_count.item()), "num_freed": int(self.num_freed.item()),
+                "affected": int(self.affected.item())}

@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): segmentation, candidate sets, block pairs, remaps, refcounts and
+free lists bit-exact; cosines bit-exact (one IEEE expression on both sides, reading R12);
+distances within 1e-5 relative (exactly 0 for identical blocks); decisions identical except
+targets within 1e-4 relative of tau_b or with a near tie, which are reported.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import kv, traces, workloads
+
+from _gpu_util import (assert_candidates_equal, assert_steps_equal, compare_decisions, compare_distances,
+                       host_pool_from_device, make_path, oracle_candidates, oracle_steps)
+
+pytestmark = pytest.mark.gpu
+
+SMALL = kv.KVShape(8, 4, 64, 16)       # several tiles per slice, quick oracle
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2507_21433_b200 import build
+    build.build()
+
+
+def full_parity(w, tau_s=None, tau_b=None, top_k=0, pairing=oracle.ALIGNED, cur_mode=oracle.CUR_ALL, cb=None, ce=None):
+    import torch
+    p = make_path(w)
+    tau_s = w.tau_s if tau_s is None else tau_s
+    tau_b = w.tau_b if tau_b is None else tau_b
+    p.autosize(tau_s, top_k, pairing, cur_mode, cb, ce)
+    p.round(tau_s, tau_b, top_k, pairing, cur_mode, cb, ce)
+    torch.cuda.synchronize()
+    assert p.read_status() == 0
+    st = oracle_steps(w)
+    assert_steps_equal(p.read_steps(), st)
+    oc = oracle_candidates(w, st, tau_s, top_k, pairing, cur_mode, cb, ce)
+    gc = p.read_candidates()
+    assert_candidates_equal(gc, oc)
+    kh, vh = host_pool_from_device(p.k_pool, p.v_pool)
+    sh = w.shape
+    pr = oc["pairs"]
+    D = oracle.block_distance(kh, vh, p.pool.layer_stride, p.pool.block_stride, sh.num_layers, sh.num_kv_heads,
+                              sh.num_kv_heads, sh.head_dim, sh.block_size, pr["target_phys"], pr["source_phys"])
+    gd = p.read_distance()
+    compare_distances(gd["distance"], D)
+    assert np.array_equal(gd["under"].astype(bool), gd["distance"] < np.float32(tau_b))
+    near = compare_decisions(gd["decisions"], D, oc["target_off"], pr["source_logical"], tau_b)
+    # remap parity on the GPU's own decisions (identical inputs to both sides)
+    s = p.read_state()
+    st_o, tab, rc, fl, fc, nf, af = oracle.remap(w.table, w.refcount, w.free_list, w.free_count, gd["decisions"],
+                                                 sh.block_size)
+    assert st_o == 0
+    assert np.array_equal(s["table"], tab) and np.array_equal(s["refcount"], rc)
+    assert np.array_equal(s["free_list"], fl) and s["free_count"] == fc
+    assert s["num_freed"] == nf and s["affected"] == af
+    return p, oc, D, near
+
+
+@pytest.mark.parametrize("eta", [0.0, 0.05])
+def test_tiny_t0(eta):
+    import json
+    import os
+    w = workloads.tiny(eta=eta)
+    p, oc, D, near = full_parity(w)
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tiny_t0.json")))
+    if eta == 0.0:
+        s = p.read_state()
+        assert s["free_list"][:s["free_count"]].tolist() == g["free_list"]
+        assert s["affected"] == g["affected_tokens"]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_small_shape_pipeline(seed):
+    w = workloads.small(SMALL, 3, 5000 + 777 * seed, seed=seed)
+    full_parity(w)
+
+
+@pytest.mark.parametrize("tau_s,top_k,pairing", [(0.9, 0, oracle.ALIGNED), (0.5, 2, oracle.ALIGNED),
+                                                 (0.8, 0, oracle.CROSS), (-1.0, 0, oracle.ALIGNED),
+                                                 (0.3, 3, oracle.CROSS)])
+def test_stage1_and_pair_variants(tau_s, top_k, pairing):
+    w = workloads.small(SMALL, 2, 2500, seed=7)
+    full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing)
+
+
+def test_online_modes():
+    w = workloads.small(SMALL, 3, 3000, seed=3)
+    full_parity(w, cur_mode=oracle.CUR_LAST)
+    full_parity(w, cur_mode=oracle.CUR_RANGE, cb=[0, 5, 10], ce=[4, 30, 11])
+
+
+def test_qwen32b_shape_two_sequences():
+    w = workloads.small(kv.QWEN32B, 2, 3100, seed=11, gen_start=128)
+    full_parity(w)
+
+
+def test_phi4_shape_sub_slices():
+    """Phi-4's 40 KiB slice is streamed as two sub-slices (n_sub = 2)."""
+    w = workloads.small(kv.PHI4, 1, 3300, seed=5, gen_start=128, vocab=traces.PHI4_VOCAB)
+    full_parity(w)
+
+
+def test_segment_edge_cases():
+    """Ragged, empty, non-final, prompt-only, delimiter-only, multi-delimiter and multi-tile
+    sequences, against the oracle."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    rng = np.random.default_rng(0)
+    seqs = [np.zeros(0, np.int32), np.asarray([5], np.int32), np.asarray([1, 1, 1], np.int32),
+            rng.choice([1, 2, 3, 4, 9], 20000, p=[0.05, 0.02, 0.31, 0.31, 0.31]).astype(np.int32),
+            rng.choice([1, 3, 4], 4097, p=[0.3, 0.35, 0.35]).astype(np.int32),
+            np.asarray([3, 3, 1, 4, 1], np.int32)]
+    toks = np.concatenate(seqs)
+    off = np.concatenate([[0], np.cumsum([s.size for s in seqs])]).astype(np.int64)
+    gs = np.asarray([0, 0, 1, 100, 0, 9], np.int32)
+    fin = np.asarray([1, 0, 1, 1, 0, 0], np.uint8)
+    delims = np.asarray([1, 2], np.int32)
+    exp = oracle.segment_steps(toks, off, gs, fin, delims)
+    dev = torch.device("cuda")
+    S = len(seqs)
+    cap = toks.size
+    out = [torch.full((cap,), -7, dtype=torch.int32, device=dev) for _ in range(3)]
+    sso = torch.zeros(S + 1, dtype=torch.int64, device=dev)
+    ws = torch.empty(L.segment_steps_workspace_size(S), dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    t = lambda a, dt: torch.as_tensor(a, dtype=dt, device=dev)
+    rc = L.segment_steps(t(toks, torch.int32), t(off, torch.int64), t(gs, torch.int32), t(fin, torch.uint8), S, delims,
+                         out[0], out[1], out[2], sso, cap, ws, status)
+    assert rc == 0
+    torch.cuda.synchronize()
+    n = int(sso[-1])
+    assert status.item() == 0
+    got = {"step_start": out[0][:n].cpu().numpy(), "step_end": out[1][:n].cpu().numpy(),
+           "step_nbag": out[2][:n].cpu().numpy(), "seq_step_off": sso.cpu().numpy()}
+    assert_steps_equal(got, exp)
+    # capacity: count-then-fill semantics
+    status.zero_()
+    rc = L.segment_steps(t(toks, torch.int32), t(off, torch.int64), t(gs, torch.int32), t(fin, torch.uint8), S, delims,
+                         out[0], out[1], out[2], sso, 10, ws, status)
+    torch.cuda.synchronize()
+    assert rc == 0 and status.item() == L.CAPACITY and int(sso[-1]) == n
+
+
+def test_long_step_uses_global_table():
+    """A 6000-token step (> 2048 content tokens) takes the global-memory hash table path."""
+    rng = np.random.default_rng(4)
+    long_step = rng.integers(10, 900, 6000).astype(np.int32)
+    toks = np.concatenate([long_step, [1], long_step[:5000], [1], rng.integers(10, 900, 3000), [1],
+                           long_step, [1]]).astype(np.int32)
+    b = traces.TraceBatch(tokens=toks, seq_tok_off=np.array([0, toks.size]), gen_start=np.zeros(1, np.int32),
+                          final=np.ones(1, np.uint8), delim_ids=np.array([1], np.int32), vocab=1000)
+    w = workloads._paged("long", SMALL, b, 1, 0.05, 0.5)
+    full_parity(w)
+
+
+def test_distance_properties_on_gpu():
+    """D(B,B) = 0 exactly, D(a,b) == D(b,a) bit for bit, and the constant-offset closed form."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    from paper_2507_21433_b200.pipeline import MemSharePath
+    sh = kv.QWEN32B
+    nb = 6
+    slice_e = sh.slice_elems
+    rng = np.random.default_rng(0)
+    base = (rng.integers(-64, 64, (sh.num_layers, 1, slice_e)) * 0.125).astype(np.float32)
+    vals = np.concatenate([base, base + np.float32(0.5), base[:, :, ::-1], base - np.float32(0.5),
+                           base * np.float32(2.0), base + np.float32(0.5)], axis=1)
+    bits = (vals.view(np.uint32) >> 16).astype(np.uint16)
+    k = torch.as_tensor(bits.view(np.int16).ravel(), device="cuda").view(torch.bfloat16)
+    vbits = ((-vals).view(np.uint32) >> 16).astype(np.uint16)      # V = -K: same squared differences
+    v = torch.as_tensor(vbits.view(np.int16).ravel(), device="cuda").view(torch.bfloat16)
+    pairs_np = np.zeros(7, L.PAIR_DTYPE)
+    tp = [1, 0, 0, 2, 0, 1, 5]
+    sp = [0, 1, 0, 0, 2, 5, 1]
+    for i in range(7):
+        pairs_np[i] = (0, i, i, 10 + i, tp[i], sp[i])
+    dims = L.Dims(sh.num_layers, sh.num_kv_heads, sh.num_kv_heads, sh.head_dim, sh.block_size)
+    pool = L.KVPool(k.data_ptr(), v.data_ptr(), nb * slice_e, slice_e, nb, 0)
+    dev = torch.device("cuda")
+    pairs = torch.as_tensor(pairs_np.view(np.uint8), device=dev)
+    toff = torch.arange(8, dtype=torch.int64, device=dev)
+    npairs = torch.tensor([7], dtype=torch.int64, device=dev)
+    ntg = torch.tensor([7], dtype=torch.int64, device=dev)
+    dist = torch.empty(7, dtype=torch.float32, device=dev)
+    under = torch.empty(7, dtype=torch.uint8, device=dev)
+    dec = torch.empty(7 * 32, dtype=torch.uint8, device=dev)
+    ws = torch.empty(L.block_distance_workspace_size(dims, 7, 7), dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    assert L.block_distance(pool, dims, pairs, toff, npairs, ntg, 7, 7, L.DIST_FULL, None, 0.3, dist, under, dec, ws,
+                            status) == 0
+    torch.cuda.synchronize()
+    D = dist.cpu().numpy()
+    assert status.item() == 0
+    assert D[2] == 0.0                                   # D(B, B) = 0
+    assert D[0] == D[1]                                  # symmetric, bit for bit
+    assert abs(D[0] - 0.5) <= 1e-6 * 0.5                 # constant offset 0.5 -> D = 0.5 (32B shape)
+    assert D[5] == 0.0 and D[6] == 0.0                   # blocks 1 and 5 are identical
+    kh = bits.ravel()
+    vh = vbits.ravel()
+    Do = oracle.block_distance(kh, vh, nb * slice_e, slice_e, sh.num_layers, sh.num_kv_heads, sh.num_kv_heads,
+                               sh.head_dim, sh.block_size, tp, sp)
+    compare_distances(D, Do)
+
+
+def test_partial_then_finalize_equals_full():
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    w = workloads.small(SMALL, 2, 4000, seed=9)
+    p = make_path(w)
+    p.autosize(w.tau_s)
+    p.segment()
+    p.candidates(w.tau_s)
+    p.alloc_partial()
+    p.distance_call(w.tau_b, L.DIST_FULL)
+    torch.cuda.synchronize()
+    full = p.read_distance()
+    ps_full = p.partial_sq.clone()
+    p.distance_call(w.tau_b, L.DIST_PARTIAL)
+    torch.cuda.synchronize()
+    assert torch.equal(p.partial_sq, ps_full)
+    p.distance.zero_()
+    p.distance_call(w.tau_b, L.DIST_FINALIZE)
+    torch.cuda.synchronize()
+    fin = p.read_distance()
+    assert np.array_equal(full["distance"], fin["distance"])
+    for k_ in full["decisions"]:
+        assert np.array_equal(full["decisions"][k_], fin["decisions"][k_])
+    # partial squares against the oracle's per-layer sums
+    oc = p.read_candidates()["pairs"]
+    kh, vh = host_pool_from_device(p.k_pool, p.v_pool)
+    sk, sv = oracle.partial_sq(kh, vh, p.pool.layer_stride, p.pool.block_stride, SMALL.num_layers,
+                               SMALL.num_kv_heads, SMALL.head_dim, SMALL.block_size, oc["target_phys"],
+                               oc["source_phys"])
+    got = p.partial_sq.cpu().numpy()[:sk.size * 2].reshape(-1, SMALL.num_layers, 2)
+    ref = np.stack([sk, sv], -1)
+    nz = ref > 0
+    assert np.all(got[~nz] == 0)
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) < 1e-5
+
+
+def test_remap_random_decisions_vs_oracle():
+    """Remap is bit-exact with the oracle on identical (random) decisions, including chains,
+    rejected entries, increments after decrements and repeated old blocks."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    rng = np.random.default_rng(1)
+    dev = torch.device("cuda")
+    for trial in range(20):
+        nseq, nblk = 4, 50
+        tab = rng.permutation(nseq * nblk).astype(np.int32).reshape(nseq, nblk)
+        tab[rng.random(tab.shape) < 0.1] = tab[0, 0]
+        rc = np.bincount(tab.ravel(), minlength=nseq * nblk).astype(np.int32)
+        fl = np.full(nseq * nblk, -1, np.int32)
+        free = np.flatnonzero(rc == 0).astype(np.int32)
+        fl[:free.size] = free
+        keys = np.unique(rng.integers(0, nseq * nblk, 60))
+        dec = np.zeros(keys.size, L.DECISION_DTYPE)
+        dec["seq"], dec["target_logical"] = keys // nblk, keys % nblk
+        dec["source_phys"] = tab.ravel()[rng.integers(0, tab.size, keys.size)]
+        dec["accepted"] = rng.random(keys.size) < 0.8
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+        dtab, drc, dfl = t(tab, torch.int32), t(rc, torch.int32), t(fl, torch.int32)
+        fc = t([free.size], torch.int64)
+        nf, af = t([0], torch.int64), t([0], torch.int64)
+        ddec = t(dec.view(np.uint8), torch.uint8)
+        nt = t([keys.size], torch.int64)
+        ws = torch.empty(L.remap_workspace_size(nseq * nblk, keys.size), dtype=torch.uint8, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        assert L.remap(dtab, nblk, nseq, drc, nseq * nblk, dfl, fc, ddec, nt, keys.size, 16, nf, af, ws, status) == 0
+        torch.cuda.synchronize()
+        st, tab2, rc2, fl2, fc2, nf2, af2 = oracle.remap(tab, rc, fl, free.size,
+                                                         {k_: dec[k_] for k_ in dec.dtype.names}, 16)
+        assert st == 0 and status.item() == 0
+        assert np.array_equal(dtab.cpu().numpy(), tab2) and np.array_equal(drc.cpu().numpy(), rc2)
+        assert np.array_equal(dfl.cpu().numpy(), fl2) and int(fc) == fc2 and int(nf) == nf2 and int(af) == af2
+
+
+def test_device_errors():
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    from paper_2507_21433_b200.pipeline import Caps
+    w = workloads.small(SMALL, 2, 3000, seed=2)
+    p = make_path(w, caps=Caps(step=w.num_tokens, match=3, pair=5, target=2))
+    p.segment()
+    p.candidates(w.tau_s)
+    torch.cuda.synchronize()
+    assert p.read_status() == L.CAPACITY
+    c = p.counts()
+    exp = oracle_candidates(w, oracle_steps(w))
+    assert c["matches"] == exp["matches"]["seq"].size and c["pairs"] == exp["pairs"]["seq"].size
+    # a corrupt physical id in the block table is reported
+    w2 = workloads.small(SMALL, 1, 3000, seed=2)
+    w2.table = w2.table.copy()
+    w2.table[0, 40:] = w2.num_blocks + 5
+    p2 = make_path(w2, with_pool=False)
+    p2.segment()
+    p2.candidates(-1.0)
+    torch.cuda.synchronize()
+    assert p2.read_status() == L.CORRUPTION
+
+
+def test_generator_twins_bit_identical():
+    w = workloads.small(SMALL, 2, 1500, seed=3)
+    p = make_path(w)
+    kh, vh = host_pool_from_device(p.k_pool, p.v_pool)
+    k2, v2, _, _ = w.host_pool()
+    assert np.array_equal(kh, k2) and np.array_equal(vh, v2)
+
+
+def test_c2_full_size_parity():
+    """configs[1] at full size, in the launch configuration bench.py times: segmentation,
+    candidates, pairs and remap bit-exact; every pair's distance against the oracle."""
+    w = workloads.c2(seed=0)
+    p, oc, D, (near_thr, near_tie) = full_parity(w)
+    assert oc["pairs"]["seq"].size > 300
+    print(f"c2: pairs={oc['pairs']['seq'].size} targets={oc['target_off'].size - 1} near_thresh={near_thr} "
+          f"near_tie={near_tie}")
