@@ -32,7 +32,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "candidate KV-block pairs scored/s"
 UNIT = "pairs/s"
-GPU_LAUNCHES_PER_STEP = 7     # seg_count, seg_fill, encode, stage1, fill, distance, remap
+GPU_LAUNCHES_PER_STEP = 9     # seg_count, seg_fill, seg_final, encode, stage1, fill, distance, finalize, remap
 
 
 def parse():
@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=int(os.environ.get("MEMSHARE_SEED", "0")))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--breakdown", action="store_true", help="also time each ABI call separately (stderr)")
+    ap.add_argument("--no-graph", action="store_true", help="launch the calls directly instead of CUDA-graph replay")
     return ap.parse_args()
 
 
@@ -242,9 +244,8 @@ def main():
     sh = w.shape
     h_local, h_off = sh.num_kv_heads, 0
     if args.mode == "headshard":
-        per = -(-sh.num_kv_heads // world)
-        h_off = min(rank * per, sh.num_kv_heads)
-        h_local = max(1, min(per, sh.num_kv_heads - h_off))
+        from paper_2507_21433_b200.sharding import head_shard
+        h_local, h_off = head_shard(sh.num_kv_heads, world, rank)
     k, v, ls, bs = w.device_pool(dev, h_local=h_local, head_offset=h_off)
     b = w.batch
     path = MemSharePath(b.tokens, b.seq_tok_off, b.gen_start, b.final, b.delim_ids, w.table, w.refcount, w.free_list,
@@ -255,30 +256,46 @@ def main():
         path.alloc_partial()
     torch.cuda.synchronize()
     pristine = {n: getattr(path, n).clone() for n in ("table", "refcount", "free_list", "free_count")}
-    stream = path.stream
+    stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
     def restore():
         for n, t in pristine.items():
             getattr(path, n).copy_(t, non_blocking=True)
 
-    def step(d_ev=None):
+    def front():                 # restore the round's initial state, a1, a2-a4
         restore()
         path.segment()
         path.candidates(w.tau_s)
-        if d_ev is not None:
-            d_ev[0].record(stream)
+
+    def middle():                # a5-a6 (the HBM-bound kernel)
         if args.mode == "headshard":
             path.distance_call(w.tau_b, L.DIST_PARTIAL)
-            n = counts["pairs"] * sh.num_layers * 2
             if world > 1:
-                dist.all_reduce(path.partial_sq[:n])
+                dist.all_reduce(path.partial_sq[:counts["pairs"] * sh.num_layers * 2])
             path.distance_call(w.tau_b, L.DIST_FINALIZE)
         else:
             path.distance_call(w.tau_b)
+
+    def back():                  # a7
+        path.remap()
+
+    for fn in (front, middle, back):      # eager warm-up (module load, attributes)
+        fn()
+    torch.cuda.synchronize()
+    if args.no_graph:
+        run = (front, middle, back)
+    else:                                  # one CUDA graph per phase; events between replays
+        run = tuple(path.capture(fn).replay for fn in (front, middle, back))
+
+    def step(d_ev=None):
+        run[0]()
+        if d_ev is not None:
+            d_ev[0].record(stream)
+        run[1]()
         if d_ev is not None:
             d_ev[1].record(stream)
-        path.remap()
+        run[2]()
 
     for _ in range(args.warmup):
         step()
@@ -293,6 +310,23 @@ def main():
     kv_bytes = U * blk_b
     meta_bytes = P * (24 + 4 + 1) + T * (8 + 32)
     alg_bytes = kv_bytes + meta_bytes
+
+    if args.breakdown:
+        calls = {"restore (torch copies)": restore, "segment_steps": path.segment,
+                 "step_candidates": lambda: path.candidates(w.tau_s),
+                 "block_distance": lambda: path.distance_call(w.tau_b), "remap": path.remap}
+        for name, fn in calls.items():
+            for _ in range(5):
+                fn()
+            ea, eb = ev(), ev()
+            ea.record(stream)
+            for _ in range(100):
+                fn()
+            eb.record(stream)
+            torch.cuda.synchronize()
+            print(f"breakdown {name}: {ea.elapsed_time(eb) / 100 * 1e3:.1f} us (eager launches)", file=sys.stderr)
+        restore()
+        torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     time.sleep(0.3)
@@ -339,7 +373,7 @@ def main():
                 "free_list": pin(w.free_list.astype(np.int32)), "free_count": pin(np.asarray([w.free_count], np.int64))}
         h2d = sum(x.numel() * x.element_size() for x in h_in.values())
         out_dec = torch.empty(path.decisions.numel(), dtype=torch.uint8).pin_memory()
-        out_tab = torch.empty(path.table.numel(), dtype=torch.int32).pin_memory()
+        out_tab = torch.empty(path.table.shape, dtype=torch.int32).pin_memory()
         out_cnt = torch.empty(5, dtype=torch.int64).pin_memory()
         d2h = out_dec.numel() + out_tab.numel() * 4 + out_cnt.numel() * 8
         cnt_dev = torch.empty(5, dtype=torch.int64, device=dev)

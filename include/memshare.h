@@ -122,8 +122,10 @@ typedef struct memshare_decision {
  * A step ends at token i when t[i] is a delimiter and t[i+1] is not (the delimiter run belongs
  * to the step it ends), or at the last token of a FINAL sequence; tokens before gen_start[s]
  * are the prompt. Only finished steps are emitted; an open tail is not a step (reading R3).
- *   tokens        int32 [seq_tok_off[num_seqs]]   concatenated token ids of all sequences
- *   seq_tok_off   int64 [num_seqs+1]             sequence s = tokens[seq_tok_off[s] .. [s+1])
+ *   tokens        int32 [num_tokens]             concatenated token ids of all sequences
+ *   num_tokens    host int64 == seq_tok_off[num_seqs] (< 2^31; sizes the tile grid)
+ *   seq_tok_off   int64 [num_seqs+1]             sequence s = tokens[seq_tok_off[s] .. [s+1]),
+ *                                                non-decreasing, seq_tok_off[0] = 0
  *   gen_start     int32 [num_seqs]               first generated position of each sequence
  *   seq_final     uint8 [num_seqs]               1 = sequence finished
  *   delim_ids_host int32 [num_delims] (host)     1..MEMSHARE_MAX_DELIMS delimiter token ids
@@ -132,14 +134,16 @@ typedef struct memshare_decision {
  *   step_nbag     int32 [step_cap]               content (non-delimiter) tokens of the step
  *   seq_step_off  int64 [num_seqs+1]             always written in full (the required size is
  *                                                seq_step_off[num_seqs]; CAPACITY if > step_cap)
+ * Implementation: tile-parallel over the flat token array (4096 tokens per CTA) with a
+ * device-wide scan of step ends, so one long sequence spreads over many SMs.
  * Errors: INVALID_ARGUMENT for null pointers, num_seqs < 0, num_delims outside 1..16, step_cap
  * < 0, a short workspace. */
-memshare_status memshare_segment_steps(const int32_t* tokens, const int64_t* seq_tok_off, const int32_t* gen_start,
-                                       const uint8_t* seq_final, int32_t num_seqs, const int32_t* delim_ids_host,
-                                       int32_t num_delims, int32_t* step_start, int32_t* step_end,
-                                       int32_t* step_nbag, int64_t* seq_step_off, int64_t step_cap, void* workspace,
-                                       size_t workspace_bytes, int32_t* device_status, void* stream);
-size_t memshare_segment_steps_workspace_size(int32_t num_seqs);
+memshare_status memshare_segment_steps(const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off,
+                                       const int32_t* gen_start, const uint8_t* seq_final, int32_t num_seqs,
+                                       const int32_t* delim_ids_host, int32_t num_delims, int32_t* step_start,
+                                       int32_t* step_end, int32_t* step_nbag, int64_t* seq_step_off, int64_t step_cap,
+                                       void* workspace, size_t workspace_bytes, int32_t* device_status, void* stream);
+size_t memshare_segment_steps_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap);
 
 /* ------------------------------------------------------------------------------------- a2-a4
  * Stage 1 + candidate block pairs (Alg. 1 Stage 1; "bag-of-words",

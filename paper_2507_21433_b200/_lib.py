@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmemshare.so")
+LIB_PATH = os.environ.get("MEMSHARE_LIB") or os.path.join(_HERE, "libmemshare.so")   # override: tuning variants only
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "memshare.h")
 
 OK, INVALID_ARGUMENT, CAPACITY, CORRUPTION, CUDA_ERROR = 0, 1, 2, 3, 4
@@ -50,9 +50,9 @@ def _load():
     L = ctypes.CDLL(LIB_PATH)
     P, I32, I64, U64, F32, F64 = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_float,
                                   ctypes.c_double)
-    L.memshare_segment_steps.argtypes = [P, P, P, P, I32, P, I32, P, P, P, P, I64, P, U64, P, P]
+    L.memshare_segment_steps.argtypes = [P, I64, P, P, P, I32, P, I32, P, P, P, P, I64, P, U64, P, P]
     L.memshare_segment_steps.restype = I32
-    L.memshare_segment_steps_workspace_size.argtypes = [I32]
+    L.memshare_segment_steps_workspace_size.argtypes = [I64, I32, I64]
     L.memshare_segment_steps_workspace_size.restype = U64
     L.memshare_step_candidates.argtypes = ([P, I64, P, I32, P, P, P, P, I64, P, I32, I32, P, P, P, I32, I32, I32, F64,
                                             I32, I32, P, I64, P, P, I64, P, P, I64, P, P, U64, P, P])
@@ -103,16 +103,16 @@ def abi_version() -> int:
 
 
 # ------------------------------------------------------------------------------------- a1
-def segment_steps_workspace_size(num_seqs: int) -> int:
-    return lib.memshare_segment_steps_workspace_size(num_seqs)
+def segment_steps_workspace_size(num_tokens: int, num_seqs: int, step_cap: int) -> int:
+    return lib.memshare_segment_steps_workspace_size(num_tokens, num_seqs, step_cap)
 
 
-def segment_steps(tokens, seq_tok_off, gen_start, seq_final, num_seqs, delim_ids, step_start, step_end, step_nbag,
-                  seq_step_off, step_cap, workspace, device_status, stream=None) -> int:
+def segment_steps(tokens, num_tokens, seq_tok_off, gen_start, seq_final, num_seqs, delim_ids, step_start, step_end,
+                  step_nbag, seq_step_off, step_cap, workspace, device_status, stream=None) -> int:
     d = np.ascontiguousarray(delim_ids, np.int32)
-    return lib.memshare_segment_steps(_ptr(tokens), _ptr(seq_tok_off), _ptr(gen_start), _ptr(seq_final), num_seqs,
-                                      d.ctypes.data, d.size, _ptr(step_start), _ptr(step_end), _ptr(step_nbag),
-                                      _ptr(seq_step_off), step_cap, _ptr(workspace),
+    return lib.memshare_segment_steps(_ptr(tokens), num_tokens, _ptr(seq_tok_off), _ptr(gen_start), _ptr(seq_final),
+                                      num_seqs, d.ctypes.data, d.size, _ptr(step_start), _ptr(step_end),
+                                      _ptr(step_nbag), _ptr(seq_step_off), step_cap, _ptr(workspace),
                                       0 if workspace is None else workspace.numel() * workspace.element_size(),
                                       _ptr(device_status), _stream(stream))
 

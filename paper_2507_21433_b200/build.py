@@ -34,5 +34,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def build_variant(name: str, defines) -> str:
+    """Tuning experiments: an extra .so with -D overrides (never the shipped library)."""
+    out = os.path.join(HERE, f"libmemshare_{name}.so")
+    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I" + os.path.join(ROOT, "include"), "-o", out,
+           *sources()]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -5,15 +5,17 @@
 // Design (B200): the bag of words of step k is never densified. The dot product with an
 // earlier step j is  <c_k, c_j> = sum over content tokens p of j of c_k[t_p],  so only the
 // CURRENT step needs a count table: an open-addressing hash table in shared memory (global
-// workspace for steps > 2048 content tokens), probed by one warp per history step while the
-// raw history tokens stream through L1/L2. Integer dot and norms are exact; the cosine is one
-// IEEE expression (__ddiv_rn / __dsqrt_rn / __dmul_rn), bit-identical to the C oracle.
+// workspace for steps > 2048 content tokens). Because steps tile the sequence, the whole
+// history of k is one contiguous token range; all threads stream it coalesced, probe k's table
+// and add hits to the dot product of the step holding the token (smem 64-bit atomics, located
+// by binary search over the staged step starts). Integer dot and norms are exact; the cosine is
+// one IEEE expression (__ddiv_rn / __dsqrt_rn / __dmul_rn), bit-identical to the C oracle.
 //
 // Three launches:
 //   encode  : one CTA per step: table -> n2 = sum count^2 (history norms)
-//   stage1  : one CTA per current step: table, warp-per-j dots, strict threshold, (cos desc,
-//             j asc) bitonic sort, top-K, stash survivors, count targets/pairs; the last CTA
-//             scans the per-step counts into output offsets
+//   stage1  : one CTA per current step: table, streamed history dots, strict threshold,
+//             (cos desc, j asc) bitonic sort, top-K, stash survivors, count targets/pairs; the
+//             last CTA scans the per-step counts into output offsets
 //   fill    : one CTA per current step: write matches, targets, target_off, pairs
 #include <cfloat>
 #include <climits>
@@ -23,7 +25,10 @@
 namespace ms {
 namespace {
 
-constexpr int kNT = 256;
+constexpr int kNT = 256;          // encode / fill
+constexpr int kNT1 = 1024;        // stage1 (one CTA per current step: widest history stream)
+constexpr int kNW1 = kNT1 / 32;
+constexpr int kUnroll = 4;
 constexpr int kNW = kNT / 32;
 constexpr int kSmemSlots = 4096;       // smem hash table (steps with <= 2048 content tokens)
 constexpr int kCandCap = 1024;         // survivors held per current step
@@ -45,6 +50,7 @@ struct CandWs {
   int64_t* off_p;
   double* stash_cos;     // [match_cap]
   int32_t* stash_j;
+  int32_t* tok_step;     // [num_tokens] global step of each token inside a finished step
   int32_t* gkeys;        // [4*num_tokens]
   int32_t* gcnts;
 };
@@ -64,6 +70,7 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   c.off_p = w.take<int64_t>(step_cap + 1);
   c.stash_cos = w.take<double>(match_cap + 1);
   c.stash_j = w.take<int32_t>(match_cap + 1);
+  c.tok_step = w.take<int32_t>(num_tokens + 1);
   c.gkeys = w.take<int32_t>(4 * num_tokens + 1);
   c.gcnts = w.take<int32_t>(4 * num_tokens + 1);
   return c;
@@ -139,12 +146,12 @@ __device__ Table build_table(const CandArgs& a, int32_t* s_keys, int32_t* s_cnts
     tb.global = true;
   }
   tb.mask = cap - 1;
-  for (uint32_t i = threadIdx.x; i < cap; i += kNT) {
+  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
     tb.keys[i] = kEmpty;
     tb.cnts[i] = 0;
   }
   __syncthreads();
-  for (int32_t p = start + threadIdx.x; p < end; p += kNT) {
+  for (int32_t p = start + threadIdx.x; p < end; p += blockDim.x) {
     const int32_t tok = t[p];
     if (is_delim(tok, a.dl)) continue;
     uint32_t slot = hash_slot(tok, tb.mask);
@@ -159,6 +166,18 @@ __device__ Table build_table(const CandArgs& a, int32_t* s_keys, int32_t* s_cnts
   }
   __syncthreads();
   return tb;
+}
+
+// smem-only probe (keys/cnts derived from the kernel's shared array -> LDS, not generic loads)
+__device__ __forceinline__ int32_t table_get_smem(const int32_t* keys, const int32_t* cnts, uint32_t mask, int32_t tok) {
+  uint32_t slot = hash_slot(tok, mask);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    const int32_t k = keys[slot];
+    if (k == tok) return cnts[slot];
+    if (k == kEmpty) return 0;
+    slot = (slot + 1) & mask;
+  }
+  return 0;
 }
 
 __device__ __forceinline__ int32_t table_get(const Table& tb, int32_t tok) {
@@ -190,6 +209,7 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
     const int32_t s = seq_of_step(a, g);
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t nbag = a.step_nbag[g];
+    for (int32_t p = a.step_start[g] + threadIdx.x; p < a.step_end[g]; p += kNT) a.ws.tok_step[tok_base + p] = (int32_t)g;
     int64_t n2 = 0;
     if (nbag > 0) {
       const Table tb = build_table(a, s_keys, s_cnts, a.tokens + tok_base, tok_base, a.step_start[g], a.step_end[g], nbag);
@@ -217,14 +237,14 @@ __device__ __forceinline__ bool cand_before(double ca, int32_t ja, double cb, in
 __device__ void sort_cands(double* cs, int32_t* js, int n) {
   if (n <= 1) return;
   const int np = (int)pow2_ceil((uint32_t)n);
-  for (int i = n + threadIdx.x; i < np; i += kNT) {
+  for (int i = n + threadIdx.x; i < np; i += blockDim.x) {
     cs[i] = -2.0;
     js[i] = INT_MAX;
   }
   __syncthreads();
   for (int k = 2; k <= np; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < np; i += kNT) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) {
         const int ixj = i ^ j;
         if (ixj > i) {
           const bool up = (i & k) == 0;
@@ -243,11 +263,11 @@ __device__ void sort_cands(double* cs, int32_t* js, int n) {
 __device__ void sort_ints(int32_t* v, int n) {
   if (n <= 1) return;
   const int np = (int)pow2_ceil((uint32_t)n);
-  for (int i = n + threadIdx.x; i < np; i += kNT) v[i] = INT_MAX;
+  for (int i = n + threadIdx.x; i < np; i += blockDim.x) v[i] = INT_MAX;
   __syncthreads();
   for (int k = 2; k <= np; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < np; i += kNT) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) {
         const int ixj = i ^ j;
         if (ixj > i) {
           const bool up = (i & k) == 0;
@@ -274,7 +294,7 @@ __device__ __forceinline__ int32_t ceil_div(int32_t a, int32_t b) { return (a + 
 
 __device__ void prepare_cands(const CandArgs& a, Cands& c, int64_t gfirst) {
   sort_ints(c.jasc, c.m);
-  for (int r = threadIdx.x; r < c.m; r += kNT) {
+  for (int r = threadIdx.x; r < c.m; r += blockDim.x) {
     const int64_t gj = gfirst + c.jasc[r];
     const int32_t lo = ceil_div(a.step_start[gj], a.block_size), hi = a.step_end[gj] / a.block_size;
     c.flo[r] = lo;
@@ -356,14 +376,17 @@ struct SelSmem {
   int32_t flo[kCandCap];
   int32_t flen[kCandCap];
   int32_t cum[kCandCap + 1];
-  int64_t sh[kNW + 1];
+  int32_t hst[kChunk];
+  int32_t hen[kChunk];
+  unsigned long long dot[kChunk];
+  int64_t sh[kNW1 + 1];
   int count;
   int overflow;
   int64_t acc_t;
   int64_t acc_p;
 };
 
-__global__ void __launch_bounds__(kNT) stage1_kernel(CandArgs a) {
+__global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -385,26 +408,51 @@ __global__ void __launch_bounds__(kNT) stage1_kernel(CandArgs a) {
     if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
     __syncthreads();
     const bool compact = a.top_k > 0 && a.top_k <= kCandCap / 2;
+    // The history of step k is the contiguous token range [start_0, end_{k-1}) of the sequence:
+    // stream it with all threads (coalesced), look each content token up in k's table and add
+    // the count to the dot product of the step that holds it (smem atomics, only for hits).
     for (int64_t jb = 0; jb < k; jb += kChunk) {
       const int64_t je = (jb + kChunk < k) ? jb + kChunk : k;
-      for (int64_t j = jb + w; j < je; j += kNW) {
-        const int64_t gj = gfirst + j;
-        if (a.step_nbag[gj] == 0) continue;              // void history step (reading R5)
-        int64_t dot = 0;
-        const int32_t e = a.step_end[gj];
-        for (int32_t p = a.step_start[gj] + lane; p < e; p += 32) {
-          const int32_t tok = t[p];
-          if (!is_delim(tok, a.dl)) dot += table_get(tb, tok);
+      const int nj = (int)(je - jb);
+      for (int i = threadIdx.x; i < nj; i += kNT1) {
+        sm.hst[i] = a.step_start[gfirst + jb + i];
+        sm.hen[i] = a.step_end[gfirst + jb + i];
+        sm.dot[i] = 0ull;
+      }
+      __syncthreads();
+      const int32_t lo = sm.hst[0], hi = sm.hen[nj - 1];
+      const int32_t* ts = a.ws.tok_step + tok_base;
+      const int64_t gjb = gfirst + jb;
+      for (int32_t base = lo + w * 32; base < hi; base += kNT1 * kUnroll) {
+        int32_t tok[kUnroll], js[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {       // issue all loads first (ILP)
+          const int32_t p = base + u * kNT1 + lane;
+          tok[u] = p < hi ? t[p] : a.dl.id[0];
+          js[u] = p < hi ? ts[p] : -1;
         }
-        dot = warp_sum(dot);
-        if (lane == 0) {
-          // sim = <v_curr, v_i> / (||v_curr|| ||v_i||), reading R12
-          const double cs = __ddiv_rn(__ll2double_rn(dot), __dsqrt_rn(__dmul_rn(n2k, __ll2double_rn(a.ws.n2[gj]))));
-          if (cs > a.tau_s) {                             // strict: "exceeding"
-            const int idx = atomicAdd(&sm.count, 1);
-            if (idx < kCandCap) { sm.cs[idx] = cs; sm.js[idx] = (int32_t)j; }
-            else sm.overflow = 1;
-          }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int32_t jl = js[u] < 0 ? -1 : (int32_t)(js[u] - gjb);
+          const bool valid = jl >= 0 && jl < nj && !is_delim(tok[u], a.dl);
+          const unsigned c = !valid ? 0u : (unsigned)(tb.global ? table_get(tb, tok[u]) : table_get_smem(sm.keys, sm.cnts, tb.mask, tok[u]));
+          // warp-aggregated accumulation: lanes of the same history step add once
+          const unsigned grp = __match_any_sync(0xffffffffu, jl);
+          const unsigned sum = __reduce_add_sync(grp, c);
+          if (sum != 0u && lane == __ffs(grp) - 1) atomicAdd(&sm.dot[jl], (unsigned long long)sum);
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < nj; i += kNT1) {
+        const int64_t gj = gfirst + jb + i;
+        if (a.step_nbag[gj] == 0) continue;                // void history step (reading R5)
+        const int64_t dot = (int64_t)sm.dot[i];
+        // sim = <v_curr, v_i> / (||v_curr|| ||v_i||), reading R12
+        const double cs = __ddiv_rn(__ll2double_rn(dot), __dsqrt_rn(__dmul_rn(n2k, __ll2double_rn(a.ws.n2[gj]))));
+        if (cs > a.tau_s) {                                // strict: "exceeding"
+          const int idx = atomicAdd(&sm.count, 1);
+          if (idx < kCandCap) { sm.cs[idx] = cs; sm.js[idx] = (int32_t)(jb + i); }
+          else sm.overflow = 1;
         }
       }
       __syncthreads();
@@ -430,7 +478,7 @@ __global__ void __launch_bounds__(kNT) stage1_kernel(CandArgs a) {
     }
     __syncthreads();
     const int64_t base = (int64_t)s_base;
-    for (int r = threadIdx.x; r < m; r += kNT) {
+    for (int r = threadIdx.x; r < m; r += kNT1) {
       if (base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
       sm.jasc[r] = sm.js[r];
     }
@@ -444,7 +492,7 @@ __global__ void __launch_bounds__(kNT) stage1_kernel(CandArgs a) {
     if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
     const int32_t* trow = a.table + (int64_t)s * a.table_stride;
     int64_t my_t = 0, my_p = 0;
-    for (int32_t i = w; i < nt; i += kNW) {
+    for (int32_t i = w; i < nt; i += kNW1) {
       const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
       my_t += kept > 0 ? 1 : 0;
       my_p += kept;
@@ -460,9 +508,9 @@ __global__ void __launch_bounds__(kNT) stage1_kernel(CandArgs a) {
     __syncthreads();
   }
   if (last_block_done(a.ws.done)) {
-    cta_scan_counts<kNT>(a.ws.cnt_m, a.ws.off_m, G, sm.sh);
-    cta_scan_counts<kNT>(a.ws.cnt_t, a.ws.off_t, G, sm.sh);
-    cta_scan_counts<kNT>(a.ws.cnt_p, a.ws.off_p, G, sm.sh);
+    cta_scan_counts<kNT1>(a.ws.cnt_m, a.ws.off_m, G, sm.sh);
+    cta_scan_counts<kNT1>(a.ws.cnt_t, a.ws.off_t, G, sm.sh);
+    cta_scan_counts<kNT1>(a.ws.cnt_p, a.ws.off_p, G, sm.sh);
     __syncthreads();
     if (threadIdx.x == 0) {
       const int64_t M = a.ws.off_m[G], T = a.ws.off_t[G], P = a.ws.off_p[G];
@@ -621,7 +669,7 @@ extern "C" memshare_status memshare_step_candidates(
   const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
   encode_kernel<<<grid_enc, kNT, 0, st>>>(a);
-  stage1_kernel<<<grid_sel, kNT, sizeof(SelSmem), st>>>(a);
+  stage1_kernel<<<grid_sel, kNT1, sizeof(SelSmem), st>>>(a);
   fill_kernel<<<grid_sel, kNT, sizeof(FillSmem), st>>>(a);
   return launch_status();
 }

@@ -16,10 +16,10 @@ struct Delims {
 };
 
 __device__ __forceinline__ bool is_delim(int32_t t, const Delims& d) {
-  bool r = false;
-#pragma unroll
-  for (int i = 0; i < MEMSHARE_MAX_DELIMS; ++i) r |= (i < d.n) && (t == d.id[i]);
-  return r;
+  if (t == d.id[0]) return true;            // the common single-delimiter case: one compare
+  for (int i = 1; i < d.n; ++i)
+    if (t == d.id[i]) return true;
+  return false;
 }
 
 // Sticky first-error device status (first writer wins).

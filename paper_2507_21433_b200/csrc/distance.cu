@@ -2,22 +2,22 @@
 // PAPER.md:237-248 (Alg. 1 Stage 2):  D = (1/N) sum_l (||K_l[Bt]-K_l[Bs]||_F + ||V_l[Bt]-V_l[Bs]||_F)/(2dh)
 // PAPER.md:268 ("small Euclidean distance are flagged as reusable"), :319-320 (minimal distance).
 //
-// B200 design (DESIGN.md §4.3). The op is a bf16 reduction bound by HBM, not a contraction: no
-// tensor cores. One persistent CTA per SM:
-//   * warp 8 (producer) takes work items (target t, layer chunk) from a global ticket, in
+// B200 design (DESIGN.md §6). The op is a bf16 reduction bound by HBM, not a contraction: no
+// tensor cores. Two launches:
+//  distance_kernel -- one persistent CTA per SM:
+//   * warp 16 (producer) takes work items (target t, layer chunk) from a global ticket, in
 //     layer-chunk-major order so that concurrently running items touch the same layers and a
-//     source block shared by several targets is re-read from L2, not HBM; for every (layer,
-//     K|V, sub-slice) it issues 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) of the target
-//     slice and then of each source slice into a 6-stage shared-memory ring, signalled through
-//     mbarrier complete_tx;
-//   * warps 0-7 (consumers) cache the target sub-slice in registers as fp32 and release its
-//     stage at once, then for each source stage compute sum (t - s)^2 with packed FFMA2 (64
+//     source block shared by several targets is re-read from L2, not HBM; it stages the item's
+//     source ids in smem with its 32 lanes and, for every (layer, K|V, sub-slice), issues 1-D
+//     TMA bulk copies (cp.async.bulk, SASS UBLKCP) of the target slice and then of each source
+//     slice into a 6-stage shared-memory ring, signalled through mbarrier complete_tx;
+//   * warps 0-15 (consumers) cache the target sub-slice in registers as fp32 and release its
+//     stage at once, then for each source stage compute sum (t - s)^2 with packed FFMA2 (32
 //     terms per thread), reduce over the warp with shuffles and store one fp32 partial per warp
-//     (no fp atomics, fixed order);
-//   * when the last layer chunk of a target completes (per-target arrival counter), that CTA
-//     finalises the target: fixed-order fp32 sums of the warp partials, fp64 sqrt / 2dh / mean,
-//     fp32 distance, the strict tau_b test and the argmin with the smaller-source-logical tie
-//     break -- all in the same launch.
+//     (no fp atomics, fixed order). Consumers never synchronise beyond the ring barriers.
+//  finalize_kernel -- one CTA per target: fixed-order fp32 sums of the warp partials, fp64 sqrt,
+//   /(2dh), layer mean, fp32 distance, the strict tau_b test and the argmin with the
+//   smaller-source-logical tie break.
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
@@ -27,13 +27,30 @@
 namespace ms {
 namespace {
 
-constexpr int kConsumerWarps = 8;
+// Tuning knobs (compile-time; defaults are the shipped configuration).
+#ifndef MS_CONSUMER_WARPS
+#define MS_CONSUMER_WARPS 16
+#endif
+#ifndef MS_STAGE_BYTES
+#define MS_STAGE_BYTES 32768
+#endif
+#ifndef MS_STAGES
+#define MS_STAGES 6
+#endif
+#ifndef MS_COPY_PIECE
+#define MS_COPY_PIECE 8192
+#endif
+#ifndef MS_DIAG_NO_COMPUTE
+#define MS_DIAG_NO_COMPUTE 0      // 1 = consumers release stages without reading them (bandwidth probe)
+#endif
+constexpr int kConsumerWarps = MS_CONSUMER_WARPS;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;
-constexpr int kStageBytes = 32768;
-constexpr int kStages = 6;
+constexpr int kStageBytes = MS_STAGE_BYTES;
+constexpr int kStages = MS_STAGES;
 constexpr int kR = kStageBytes / 16 / kConsumers;   // uint4 chunks per consumer thread per stage
-constexpr int kCopyPiece = 8192;
+constexpr int kCopyPiece = MS_COPY_PIECE;
+constexpr int kMaxStagedPairs = 1024;   // source ids staged in smem per item
 
 constexpr int F_TARGET = 1, F_ITEM_END = 2, F_STOP = 4, F_SKIP = 8;
 
@@ -50,14 +67,12 @@ struct Meta {
 
 struct DistWs {
   unsigned int* ticket;
-  unsigned int* tdone;   // [target_cap]
   float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]
 };
 
 DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int64_t pair_cap, int64_t target_cap) {
   DistWs d;
   d.ticket = w.take<unsigned int>(1);
-  d.tdone = w.take<unsigned int>(target_cap + 1);
   d.wpart = w.take<float>((size_t)pair_cap * N * 2 * n_sub * kConsumerWarps + 1);
   return d;
 }
@@ -91,8 +106,7 @@ struct DistSmem {
   alignas(8) uint64_t full[kStages];
   uint64_t empty[kStages];
   Meta meta[kStages];
-  double terms[kConsumers];
-  int fin;
+  int32_t src_phys[kMaxStagedPairs];
 };
 
 // ------------------------------------------------------------------------- PTX helpers
@@ -125,7 +139,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
 __device__ __forceinline__ float2 bf2_to_f2(uint32_t x) {
   return make_float2(__uint_as_float(x << 16), __uint_as_float(x & 0xFFFF0000u));
@@ -238,62 +251,77 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------------ producer warp
-    if (lane == 0) {
-      const int64_t T = clamp_count(a.num_targets, a.target_cap);
-      const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
-      const int64_t total = T * a.n_chunks;
-      int stage = 0;
-      uint32_t ph = 0;
-      auto push = [&](const Meta& m, const uint8_t* src) {
-        mbar_wait(&sm.empty[stage], ph ^ 1u);
-        sm.meta[stage] = m;
-        if (src != nullptr) {
-          mbar_expect_tx(&sm.full[stage], (uint32_t)m.bytes);
-          for (int off = 0; off < m.bytes; off += kCopyPiece) {
-            const int nb = (m.bytes - off) < kCopyPiece ? (m.bytes - off) : kCopyPiece;
-            bulk_g2s(sm.ring[stage] + off, src + off, (uint32_t)nb, &sm.full[stage]);
-          }
-        } else {
-          mbar_arrive(&sm.full[stage]);
+    // All 32 lanes stage the item's source ids into smem (one coalesced round trip instead of
+    // a dependent global load per copy) and lane 0 fetches the next ticket while the current
+    // item's copies are issued, so the ring never waits on metadata latency.
+    const int64_t T = clamp_count(a.num_targets, a.target_cap);
+    const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
+    const int64_t total = T * a.n_chunks;
+    int stage = 0;
+    uint32_t ph = 0;
+    auto push = [&](const Meta& m, const uint8_t* src) {
+      mbar_wait(&sm.empty[stage], ph ^ 1u);
+      sm.meta[stage] = m;
+      if (src != nullptr) {
+        mbar_expect_tx(&sm.full[stage], (uint32_t)m.bytes);
+        for (int off = 0; off < m.bytes; off += kCopyPiece) {
+          const int nb = (m.bytes - off) < kCopyPiece ? (m.bytes - off) : kCopyPiece;
+          bulk_g2s(sm.ring[stage] + off, src + off, (uint32_t)nb, &sm.full[stage]);
         }
-        if (++stage == kStages) { stage = 0; ph ^= 1u; }
-      };
-      for (;;) {
-        const int64_t item = (int64_t)atomicAdd(a.ws.ticket, 1u);
-        if (item >= total) break;
-        const int64_t lc = item / T, t = item - lc * T;
-        const int64_t p0 = __ldcg(a.target_off + t);
-        int64_t p1 = __ldcg(a.target_off + t + 1);
-        if (p1 > P) p1 = P;
+      } else {
+        mbar_arrive(&sm.full[stage]);
+      }
+      if (++stage == kStages) { stage = 0; ph ^= 1u; }
+    };
+    int64_t item = 0;
+    if (lane == 0) item = (int64_t)atomicAdd(a.ws.ticket, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    while (item < total) {
+      int64_t next = 0;
+      if (lane == 0) next = (int64_t)atomicAdd(a.ws.ticket, 1u);   // consumed at the end of the item
+      const int64_t lc = item / T, t = item - lc * T;
+      const int64_t p0 = __ldcg(a.target_off + t);
+      int64_t p1 = __ldcg(a.target_off + t + 1);
+      if (p1 > P) p1 = P;
+      const int64_t np = p1 - p0;
+      for (int64_t q = lane; q < np && q < kMaxStagedPairs; q += 32)
+        sm.src_phys[q] = checked_phys(a, a.pairs[p0 + q].source_phys);
+      const int32_t tphys = np > 0 ? checked_phys(a, a.pairs[p0].target_phys) : 0;
+      __syncwarp();
+      if (lane == 0) {
         Meta m{};
         m.target = t;
-        if (p1 <= p0) {
+        if (np <= 0) {
           m.pair = -1; m.flags = F_ITEM_END | F_SKIP;
           push(m, nullptr);
-          continue;
-        }
-        const int32_t tphys = checked_phys(a, a.pairs[p0].target_phys);
-        const int32_t l0 = (int32_t)lc * a.lpi;
-        const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
-        for (int32_t l = l0; l < l1; ++l) {
-          for (int32_t kv = 0; kv < 2; ++kv) {
-            const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
-            for (int32_t sub = 0; sub < a.n_sub; ++sub) {
-              const int32_t off = sub * a.sub_bytes;
-              const int32_t bytes = (a.slice_bytes - off) < a.sub_bytes ? (a.slice_bytes - off) : a.sub_bytes;
-              m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes;
-              m.pair = -1; m.flags = F_TARGET;
-              push(m, base + (int64_t)tphys * a.block_stride_b + off);
-              for (int64_t p = p0; p < p1; ++p) {
-                const int32_t sphys = checked_phys(a, a.pairs[p].source_phys);
-                m.pair = p;
-                m.flags = (l == l1 - 1 && kv == 1 && sub == a.n_sub - 1 && p == p1 - 1) ? F_ITEM_END : 0;
-                push(m, base + (int64_t)sphys * a.block_stride_b + off);
+        } else {
+          const int32_t l0 = (int32_t)lc * a.lpi;
+          const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
+          for (int32_t l = l0; l < l1; ++l) {
+            for (int32_t kv = 0; kv < 2; ++kv) {
+              const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
+              for (int32_t sub = 0; sub < a.n_sub; ++sub) {
+                const int32_t off = sub * a.sub_bytes;
+                const int32_t bytes = (a.slice_bytes - off) < a.sub_bytes ? (a.slice_bytes - off) : a.sub_bytes;
+                m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes;
+                m.pair = -1; m.flags = F_TARGET;
+                push(m, base + (int64_t)tphys * a.block_stride_b + off);
+                for (int64_t q = 0; q < np; ++q) {
+                  const int32_t sphys = q < kMaxStagedPairs ? sm.src_phys[q]
+                                                            : checked_phys(a, a.pairs[p0 + q].source_phys);
+                  m.pair = p0 + q;
+                  m.flags = (l == l1 - 1 && kv == 1 && sub == a.n_sub - 1 && q == np - 1) ? F_ITEM_END : 0;
+                  push(m, base + (int64_t)sphys * a.block_stride_b + off);
+                }
               }
             }
           }
         }
       }
+      __syncwarp();
+      item = __shfl_sync(0xffffffffu, next, 0);
+    }
+    if (lane == 0) {
       Meta stop{};
       stop.flags = F_STOP;
       push(stop, nullptr);
@@ -309,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
     mbar_wait(&sm.full[stage], ph);
     const Meta m = sm.meta[stage];
     if (m.flags & F_STOP) break;
-    if (!(m.flags & F_SKIP)) {
+    if (!(m.flags & F_SKIP) && !MS_DIAG_NO_COMPUTE) {
       const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
       const int nchunk = m.bytes >> 4;
       if (m.flags & F_TARGET) {
@@ -351,27 +379,17 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[stage]);
     if (++stage == kStages) { stage = 0; ph ^= 1u; }
-
-    if (m.flags & F_ITEM_END) {
-      __threadfence();
-      consumer_bar();
-      if (tid == 0) {
-        const unsigned int old = atomicAdd(a.ws.tdone + m.target, 1u);
-        sm.fin = (old == (unsigned int)(a.n_chunks - 1)) ? 1 : 0;
-        __threadfence();
-      }
-      consumer_bar();
-      if (sm.fin) finalize_target(a, m.target, sm.terms, tid, false, [] { consumer_bar(); });
-    }
   }
 }
 
-// FINALIZE mode: one CTA per target (grid-stride), partial sums already reduced across ranks.
-__global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a) {
+// Finalisation: one CTA per target (grid-stride). FULL/PARTIAL read the per-warp partials the
+// streaming kernel left in the workspace (kernel boundary = the only synchronisation needed);
+// FINALIZE reads partial squared sums already reduced across ranks.
+__global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int from_partial) {
   __shared__ double terms[kConsumers];
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
   for (int64_t t = blockIdx.x; t < T; t += gridDim.x)
-    finalize_target(a, t, terms, threadIdx.x, true, [] { __syncthreads(); });
+    finalize_target(a, t, terms, threadIdx.x, from_partial != 0, [] { __syncthreads(); });
 }
 
 }  // namespace
@@ -449,10 +467,10 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   a.ws = dist_layout(w, a.N, a.n_sub, pair_cap, target_cap);
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t tc = target_cap < 1 ? 1 : target_cap;
+  const int fin_grid = (int)(tc < 8 * sm_count() ? tc : 8 * sm_count());
   if (mode == MEMSHARE_DIST_FINALIZE) {
-    const int64_t tc = target_cap < 1 ? 1 : target_cap;
-    const int grid = (int)(tc < 8 * sm_count() ? tc : 8 * sm_count());
-    finalize_kernel<<<grid, kConsumers, 0, st>>>(a);
+    finalize_kernel<<<fin_grid, kConsumers, 0, st>>>(a, 1);
     return launch_status();
   }
   static bool attr_set = false;
@@ -462,9 +480,8 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
       return MEMSHARE_ERR_CUDA;
     attr_set = true;
   }
-  // ticket and per-target arrival counters (adjacent at the front of the workspace)
-  const size_t ctl = reinterpret_cast<char*>(a.ws.tdone + target_cap + 1) - reinterpret_cast<char*>(a.ws.ticket);
-  if (cudaMemsetAsync(a.ws.ticket, 0, ctl, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  if (cudaMemsetAsync(a.ws.ticket, 0, sizeof(unsigned int), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   distance_kernel<<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
+  finalize_kernel<<<fin_grid, kConsumers, 0, st>>>(a, 0);
   return launch_status();
 }

@@ -39,7 +39,7 @@ class MemSharePath:
                  k_pool, v_pool, layer_stride, block_stride, num_blocks, num_layers, h_local, h_global, head_dim,
                  block_size, caps: Caps | None = None, device="cuda", stream=None):
         self.dev = torch.device(device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self._stream = stream      # None: every call goes to the then-current stream (CUDA-graph capture works)
         self.delims = np.ascontiguousarray(delim_ids, np.int32)
         self.num_seqs = int(len(gen_start))
         self.num_tokens = int(len(tokens))
@@ -69,6 +69,22 @@ class MemSharePath:
         self.set_caps(caps or Caps(step=max(1, self.num_tokens), match=max(1024, self.num_tokens),
                                    pair=max(4096, self.num_tokens), target=max(2048, self.num_tokens // block_size + 1)))
 
+    @property
+    def stream(self):
+        return self._stream if self._stream is not None else torch.cuda.current_stream(self.dev)
+
+    def capture(self, fn):
+        """Capture `fn` (a sequence of the calls above) into a CUDA graph; returns the graph
+        (replay() re-runs the captured launches with the same buffers)."""
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                fn()
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        return g
+
     # ------------------------------------------------------------------ buffers
     def set_caps(self, caps: Caps):
         self.caps = caps
@@ -81,7 +97,7 @@ class MemSharePath:
         self.distance = e(caps.pair, torch.float32)
         self.under = e(caps.pair, torch.uint8)
         self.decisions = e(caps.target * 32, torch.uint8)
-        ws = max(L.segment_steps_workspace_size(self.num_seqs),
+        ws = max(L.segment_steps_workspace_size(self.num_tokens, self.num_seqs, caps.step),
                  L.step_candidates_workspace_size(self.num_tokens, self.num_seqs, caps.step, caps.match),
                  L.block_distance_workspace_size(self.dims, caps.pair, caps.target),
                  L.remap_workspace_size(self.num_blocks, caps.target))
@@ -94,7 +110,8 @@ class MemSharePath:
 
     # ------------------------------------------------------------------ the four calls
     def segment(self):
-        L.check(L.segment_steps(self.tokens, self.seq_tok_off, self.gen_start, self.final, self.num_seqs, self.delims,
+        L.check(L.segment_steps(self.tokens, self.num_tokens, self.seq_tok_off, self.gen_start, self.final,
+                                self.num_seqs, self.delims,
                                 self.step_start, self.step_end, self.step_nbag, self.seq_step_off, self.caps.step,
                                 self.workspace, self.status, self.stream), "segment_steps")
 

@@ -54,7 +54,7 @@ def test_status_strings_and_version(lib):
 
 
 def test_workspace_sizes_are_host_only(lib):
-    assert lib.segment_steps_workspace_size(10) > 0
+    assert lib.segment_steps_workspace_size(1000, 10, 100) > 0
     assert lib.step_candidates_workspace_size(1000, 2, 100, 50) > lib.step_candidates_workspace_size(10, 2, 100, 50)
     d = lib.Dims(64, 8, 8, 128, 16)
     assert lib.block_distance_workspace_size(d, 100, 10) >= 100 * 64 * 2 * 8 * 4
@@ -66,8 +66,8 @@ def test_invalid_arguments_rejected_before_any_launch(lib):
     nul = None
     # null pointers / bad counts -> INVALID_ARGUMENT (1), nothing enqueued
     d = (ctypes.c_int32 * 1)(5)
-    assert L.memshare_segment_steps(nul, nul, nul, nul, 1, d, 1, nul, nul, nul, nul, 0, nul, 0, nul, nul) == 1
-    assert L.memshare_segment_steps(nul, nul, nul, nul, 1, d, 0, nul, nul, nul, nul, 0, nul, 0, nul, nul) == 1
+    assert L.memshare_segment_steps(nul, 0, nul, nul, nul, 1, d, 1, nul, nul, nul, nul, 0, nul, 0, nul, nul) == 1
+    assert L.memshare_segment_steps(nul, 0, nul, nul, nul, 1, d, 0, nul, nul, nul, nul, 0, nul, 0, nul, nul) == 1
     dims = lib.Dims(64, 8, 8, 12, 16)        # head_dim % 8 != 0
     assert L.memshare_block_distance(nul, ctypes.byref(dims), nul, nul, nul, nul, 0, 0, 0, nul, 0.1, nul, nul, nul,
                                      nul, 0, nul, nul) == 1
