@@ -205,7 +205,8 @@ memshare_status memshare_block_distance(const memshare_kv_pool* pool_host, const
                                         float* distance, uint8_t* under, memshare_decision* decisions,
                                         void* workspace, size_t workspace_bytes, int32_t* device_status,
                                         void* stream);
-size_t memshare_block_distance_workspace_size(const memshare_dims* dims_host, int64_t pair_cap, int64_t target_cap);
+size_t memshare_block_distance_workspace_size(const memshare_dims* dims_host, int32_t num_blocks, int64_t pair_cap,
+                                              int64_t target_cap);
 
 /* ---------------------------------------------------------------------------------------- a7
  * Zero-copy remap (PAPER.md:276-278 "the mechanism simply updates the block table", :283-284;

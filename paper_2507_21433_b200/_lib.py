@@ -61,7 +61,7 @@ def _load():
     L.memshare_step_candidates_workspace_size.restype = U64
     L.memshare_block_distance.argtypes = [P, P, P, P, P, P, I64, I64, I32, P, F32, P, P, P, P, U64, P, P]
     L.memshare_block_distance.restype = I32
-    L.memshare_block_distance_workspace_size.argtypes = [P, I64, I64]
+    L.memshare_block_distance_workspace_size.argtypes = [P, I32, I64, I64]
     L.memshare_block_distance_workspace_size.restype = U64
     L.memshare_remap.argtypes = [P, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, P, U64, P, P]
     L.memshare_remap.restype = I32
@@ -137,8 +137,8 @@ def step_candidates(tokens, num_tokens, seq_tok_off, num_seqs, seq_step_off, ste
 
 
 # ----------------------------------------------------------------------------------- a5-a6
-def block_distance_workspace_size(dims: Dims, pair_cap: int, target_cap: int) -> int:
-    return lib.memshare_block_distance_workspace_size(ctypes.byref(dims), pair_cap, target_cap)
+def block_distance_workspace_size(dims: Dims, num_blocks: int, pair_cap: int, target_cap: int) -> int:
+    return lib.memshare_block_distance_workspace_size(ctypes.byref(dims), num_blocks, pair_cap, target_cap)
 
 
 def block_distance(pool: KVPool | None, dims: Dims, pairs, target_off, num_pairs, num_targets, pair_cap, target_cap,

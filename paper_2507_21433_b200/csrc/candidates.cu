@@ -19,6 +19,7 @@
 //   fill    : one CTA per current step: write matches, targets, target_off, pairs
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -106,6 +107,7 @@ struct CandArgs {
   int64_t target_cap;
   int64_t* num_targets;
   int32_t* status;
+  int32_t dbg_skip;     // tuning only (env MEMSHARE_DEBUG_SKIP): bit0 history stream, bit1 pair count, bit2 last-CTA scan
   CandWs ws;
 };
 
@@ -367,6 +369,20 @@ __device__ __forceinline__ bool is_current(const CandArgs& a, int32_t s, int64_t
   return k >= a.cur_begin[s] && k < a.cur_end[s];
 }
 
+// Tuning only (MEMSHARE_DEBUG_SKIP bit 3): per-CTA phase timestamps of stage1 (globaltimer ns).
+constexpr int kDbgSlots = 16;
+__device__ unsigned long long g_dbg_t[2048 * kDbgSlots];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define DBG_T(slot)                                                                         \
+  do {                                                                                      \
+    if ((a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)                          \
+      g_dbg_t[blockIdx.x * kDbgSlots + (slot)] = gtimer();                                  \
+  } while (0)
+
 struct SelSmem {
   int32_t keys[kSmemSlots];
   int32_t cnts[kSmemSlots];
@@ -390,6 +406,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  DBG_T(0);
   const int64_t G = total_steps(a);
   for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
     const int32_t s = a.ws.step_seq[g];
@@ -404,6 +421,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t* t = a.tokens + tok_base;
     const Table tb = build_table(a, sm.keys, sm.cnts, t, tok_base, a.step_start[g], a.step_end[g], nbag);
+    DBG_T(1);
     const double n2k = (double)a.ws.n2[g];
     if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
     __syncthreads();
@@ -423,7 +441,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       const int32_t lo = sm.hst[0], hi = sm.hen[nj - 1];
       const int32_t* ts = a.ws.tok_step + tok_base;
       const int64_t gjb = gfirst + jb;
-      for (int32_t base = lo + w * 32; base < hi; base += kNT1 * kUnroll) {
+      for (int32_t base = lo + w * 32; base < hi && !(a.dbg_skip & 1); base += kNT1 * kUnroll) {
         int32_t tok[kUnroll], js[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {       // issue all loads first (ILP)
@@ -463,6 +481,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
         __syncthreads();
       }
     }
+    DBG_T(2);
     if (sm.overflow) {
       if (threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
       __syncthreads();
@@ -470,6 +489,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
     int m = sm.count < kCandCap ? sm.count : kCandCap;
     sort_cands(sm.cs, sm.js, m);
     if (a.top_k > 0 && m > a.top_k) m = a.top_k;
+    DBG_T(3);
     // stash the ranked survivors for the fill kernel
     __shared__ unsigned long long s_base;
     if (threadIdx.x == 0) {
@@ -485,20 +505,23 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
     if (threadIdx.x == 0) { sm.acc_t = 0; sm.acc_p = 0; }
     __syncthreads();
     // a4: count targets and deduplicated pairs of this step
+    DBG_T(4);
     Cands c{m, sm.jasc, sm.flo, sm.flen, sm.cum};
     prepare_cands(a, c, gfirst);
+    DBG_T(5);
     const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
     const int32_t nt = (m > 0 && fk_hi > fk_lo) ? fk_hi - fk_lo : 0;
     if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
     const int32_t* trow = a.table + (int64_t)s * a.table_stride;
     int64_t my_t = 0, my_p = 0;
-    for (int32_t i = w; i < nt; i += kNW1) {
+    for (int32_t i = w; i < nt && !(a.dbg_skip & 2); i += kNW1) {
       const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
       my_t += kept > 0 ? 1 : 0;
       my_p += kept;
     }
     if (lane == 0) { atomicAdd((unsigned long long*)&sm.acc_t, (unsigned long long)my_t); atomicAdd((unsigned long long*)&sm.acc_p, (unsigned long long)my_p); }
     __syncthreads();
+    DBG_T(6);
     if (threadIdx.x == 0) {
       a.ws.cnt_m[g] = m;
       a.ws.cnt_t[g] = (int32_t)sm.acc_t;
@@ -507,7 +530,9 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
     }
     __syncthreads();
   }
-  if (last_block_done(a.ws.done)) {
+  DBG_T(7);
+  if (!(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
+    DBG_T(8);
     cta_scan_counts<kNT1>(a.ws.cnt_m, a.ws.off_m, G, sm.sh);
     cta_scan_counts<kNT1>(a.ws.cnt_t, a.ws.off_t, G, sm.sh);
     cta_scan_counts<kNT1>(a.ws.cnt_p, a.ws.off_p, G, sm.sh);
@@ -520,6 +545,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       if (M > a.match_cap || T > a.target_cap || P > a.pair_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
       if (T <= a.target_cap) a.target_off[T] = P;
     }
+    DBG_T(9);
   }
 }
 
@@ -604,6 +630,12 @@ __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
 
 using namespace ms;
 
+// Tuning only, not part of the public ABI: copy the stage1 phase timestamps to the host.
+extern "C" int memshare_debug_stage1_times(unsigned long long* host, int n) {
+  if (n > 2048 * kDbgSlots) n = 2048 * kDbgSlots;
+  return (int)cudaMemcpyFromSymbol(host, g_dbg_t, (size_t)n * sizeof(unsigned long long));
+}
+
 extern "C" size_t memshare_step_candidates_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap,
                                                           int64_t match_cap) {
   if (num_tokens < 0 || num_seqs < 0 || step_cap < 0 || match_cap < 0) return 0;
@@ -651,6 +683,11 @@ extern "C" memshare_status memshare_step_candidates(
   a.pairs = pairs; a.pair_cap = pair_cap; a.num_pairs = num_pairs;
   a.target_off = target_off; a.target_cap = target_cap; a.num_targets = num_targets;
   a.status = device_status;
+  {
+    static int dbg = -1;
+    if (dbg < 0) { const char* e = getenv("MEMSHARE_DEBUG_SKIP"); dbg = e ? atoi(e) : 0; }
+    a.dbg_skip = dbg;
+  }
   Ws w{static_cast<char*>(workspace), 0};
   a.ws = cand_layout(w, num_tokens, step_cap, match_cap);
 
@@ -668,8 +705,9 @@ extern "C" memshare_status memshare_step_candidates(
   const int64_t gcap = step_cap < 1 ? 1 : step_cap;
   const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
+  const int grid_s1 = (int)(gcap < sms ? gcap : sms);      // 1024-thread CTAs: one per SM, one wave
   encode_kernel<<<grid_enc, kNT, 0, st>>>(a);
-  stage1_kernel<<<grid_sel, kNT1, sizeof(SelSmem), st>>>(a);
+  stage1_kernel<<<grid_s1, kNT1, sizeof(SelSmem), st>>>(a);
   fill_kernel<<<grid_sel, kNT, sizeof(FillSmem), st>>>(a);
   return launch_status();
 }

@@ -3,18 +3,23 @@
 // PAPER.md:268 ("small Euclidean distance are flagged as reusable"), :319-320 (minimal distance).
 //
 // B200 design. The op is a bf16 reduction bound by HBM, not a contraction: no
-// tensor cores. Two launches:
-//  distance_kernel -- one persistent CTA per SM:
-//   * warp 16 (producer) takes work items (target t, layer chunk) from a global ticket, in
-//     layer-chunk-major order so that concurrently running items touch the same layers and a
-//     source block shared by several targets is re-read from L2, not HBM; it stages the item's
-//     source ids in smem with its 32 lanes and, for every (layer, K|V, sub-slice), issues 1-D
-//     TMA bulk copies (cp.async.bulk, SASS UBLKCP) of the target slice and then of each source
-//     slice into a 6-stage shared-memory ring, signalled through mbarrier complete_tx;
-//   * warps 0-15 (consumers) cache the target sub-slice in registers as fp32 and release its
-//     stage at once, then for each source stage compute sum (t - s)^2 with packed FFMA2 (32
-//     terms per thread), reduce over the warp with shuffles and store one fp32 partial per warp
-//     (no fp atomics, fixed order). Consumers never synchronise beyond the ring barriers.
+// tensor cores. Three launches:
+//  plan_kernel -- one CTA: targets sorted by (first source block, index) in shared memory
+//   (bitonic); runs of <= kAnchors targets with the same first source become ITEMS (<= 64 pairs).
+//   Near-copies of one earlier step (redundant thinking) pair with the same
+//   source blocks, so the targets of an item share most of their sources.
+//  distance_kernel -- one persistent CTA per SM, warp-specialised:
+//   * warp 16 (producer) takes (item, layer chunk) units from a global ticket, layer-chunk-major
+//     so that all SMs work on the same layers at a time (the per-layer working set stays in
+//     L2); for every (layer, K|V, sub-slice) it issues one 1-D TMA bulk copy (cp.async.bulk,
+//     SASS UBLKCP) per ANCHOR (the item's targets) and then one per DISTINCT source of the item
+//     into a 6-stage 32 KiB shared-memory ring, completed through mbarrier transaction counts;
+//     each stage carries the list of pairs to evaluate against it;
+//   * warps 0-15 (consumers) copy each stage into registers and release it at once; anchors stay
+//     in registers (bf16, 4 x 16 regs); every other stage is evaluated against the anchors its
+//     pairs name: d = t - s (FFMA2, exactly rounded), acc += d*d (FFMA2, fp32, 32 terms per
+//     thread), warp-shuffle sum, one fp32 partial per warp (fixed order, no fp atomics).
+//   A source shared by several targets of an item crosses HBM->SMEM once per item.
 //  finalize_kernel -- one CTA per target: fixed-order fp32 sums of the warp partials, fp64 sqrt,
 //   /(2dh), layer mean, fp32 distance, the strict tau_b test and the argmin with the
 //   smaller-source-logical tie break.
@@ -29,7 +34,7 @@ namespace {
 
 // Tuning knobs (compile-time; defaults are the shipped configuration).
 #ifndef MS_CONSUMER_WARPS
-#define MS_CONSUMER_WARPS 16
+#define MS_CONSUMER_WARPS 8
 #endif
 #ifndef MS_STAGE_BYTES
 #define MS_STAGE_BYTES 32768
@@ -37,42 +42,67 @@ namespace {
 #ifndef MS_STAGES
 #define MS_STAGES 6
 #endif
-#ifndef MS_COPY_PIECE
-#define MS_COPY_PIECE 8192
-#endif
 #ifndef MS_DIAG_NO_COMPUTE
 #define MS_DIAG_NO_COMPUTE 0      // 1 = consumers release stages without reading them (bandwidth probe)
 #endif
+#ifndef MS_ANCHORS
+#define MS_ANCHORS 1
+#endif
+#ifndef MS_ANCHOR_FP32
+#define MS_ANCHOR_FP32 1          // 1: anchors cached as fp32 (2x registers, no per-pair unpack)
+#endif
 constexpr int kConsumerWarps = MS_CONSUMER_WARPS;
+static_assert(kConsumerWarps % 4 == 0, "partials are read as float4");
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;
 constexpr int kStageBytes = MS_STAGE_BYTES;
 constexpr int kStages = MS_STAGES;
 constexpr int kR = kStageBytes / 16 / kConsumers;   // uint4 chunks per consumer thread per stage
-constexpr int kCopyPiece = MS_COPY_PIECE;
-constexpr int kMaxStagedPairs = 1024;   // source ids staged in smem per item
+static_assert(kR * 16 * kConsumers == kStageBytes, "stage must split evenly over consumers");
+constexpr int kAnchors = MS_ANCHORS;                // targets (anchors) per item
+static_assert(kAnchors >= 1 && kAnchors <= 4, "anchor registers are unrolled for <= 4");
+constexpr int kItemPairs = 64;                      // pairs per item
+constexpr int kMetaEnt = 4;                         // pairs evaluated against one stage
+constexpr int kPlanThreads = 1024;
 
-constexpr int F_TARGET = 1, F_ITEM_END = 2, F_STOP = 4, F_SKIP = 8;
+constexpr int F_STOP = 1;
 
+// One work item: <= kAnchors targets of one pair-graph component, with the pair range of each.
+struct ItemRec {
+  int32_t na;
+  int32_t tgt[kAnchors];
+  int32_t lo[kAnchors];
+  int32_t hi[kAnchors];
+};
+
+// One ring stage: which slice it holds and which pairs to evaluate against it.
 struct Meta {
-  int64_t pair;
-  int64_t target;
-  int32_t layer;
-  int32_t kv;
-  int32_t sub;
-  int32_t bytes;
-  int32_t flags;
-  int32_t pad;
+  int32_t pair[kMetaEnt];
+  int8_t anc[kMetaEnt];    // anchor slot holding the other operand of pair[e]
+  int32_t nent;
+  int32_t anchor;          // >= 0: this slice becomes anchor slot `anchor`
+  int32_t layer, kv, sub, bytes, flags;
 };
 
 struct DistWs {
   unsigned int* ticket;
+  int64_t* n_items;
+  ItemRec* items;        // [item_cap]
+  int32_t* cnt;          // [target_cap] items starting at each sorted position
+  int64_t* item_off;     // [target_cap + 1]
   float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]
 };
 
-DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int64_t pair_cap, int64_t target_cap) {
+int64_t item_cap_of(int64_t pair_cap, int64_t target_cap) { return target_cap + pair_cap / kItemPairs + 2; }
+
+DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t num_blocks, int64_t pair_cap, int64_t target_cap) {
+  (void)num_blocks;
   DistWs d;
   d.ticket = w.take<unsigned int>(1);
+  d.n_items = w.take<int64_t>(1);
+  d.items = w.take<ItemRec>(item_cap_of(pair_cap, target_cap));
+  d.cnt = w.take<int32_t>(target_cap + 1);
+  d.item_off = w.take<int64_t>(target_cap + 2);
   d.wpart = w.take<float>((size_t)pair_cap * N * 2 * n_sub * kConsumerWarps + 1);
   return d;
 }
@@ -86,6 +116,7 @@ struct DistArgs {
   int32_t N, d, h_global;
   int32_t slice_bytes, n_sub, sub_bytes;
   int32_t lpi, n_chunks;
+  int32_t plan_sort_cap;     // targets the planner can sort in its shared memory
   const memshare_block_pair* pairs;
   const int64_t* target_off;
   const int64_t* num_pairs;
@@ -101,12 +132,32 @@ struct DistArgs {
   DistWs ws;
 };
 
+constexpr int kMaxTemplates = 2 * kAnchors + 2 * kItemPairs;
+
+struct StageTpl {             // one stage of an item, the same for every (layer, K|V, sub-slice)
+  int32_t phys;
+  int32_t anchor;
+  int32_t nent;
+  int32_t pair[kMetaEnt];
+  int8_t anc[kMetaEnt];
+};
+
+struct ProdSmem {               // producer-private staging of one item
+  int32_t ent_pair[kItemPairs];
+  int32_t ent_phys[kItemPairs];
+  int8_t ent_anc[kItemPairs];
+  int8_t ent_kind[kItemPairs];   // -1: streamed (first of its phys); -2: streamed duplicate; >= 0: anchor
+  int32_t aphys[kAnchors];
+  StageTpl tpl[kMaxTemplates];
+  int32_t ntpl;
+};
+
 struct DistSmem {
   alignas(128) uint8_t ring[kStages][kStageBytes];
   alignas(8) uint64_t full[kStages];
   uint64_t empty[kStages];
   Meta meta[kStages];
-  int32_t src_phys[kMaxStagedPairs];
+  ProdSmem prod;
 };
 
 // ------------------------------------------------------------------------- PTX helpers
@@ -152,9 +203,15 @@ __device__ __forceinline__ int64_t clamp_count(const int64_t* p, int64_t cap) {
 // fixed-order fp32 sum of the per-warp partials of (pair p, layer l, kv)
 __device__ __forceinline__ float sum_part(const DistArgs& a, int64_t p, int32_t l, int32_t kv, bool from_partial) {
   if (from_partial) return __ldcg(a.partial_sq + ((p * a.N + l) * 2 + kv));
-  const float* w = a.ws.wpart + (((p * a.N + l) * 2 + kv) * a.n_sub) * kConsumerWarps;
+  const float4* w = reinterpret_cast<const float4*>(a.ws.wpart + (((p * a.N + l) * 2 + kv) * a.n_sub) * kConsumerWarps);
   float s = 0.f;
-  for (int j = 0; j < a.n_sub * kConsumerWarps; ++j) s += __ldcg(w + j);
+  for (int sub = 0; sub < a.n_sub; ++sub) {
+    float4 v[kConsumerWarps / 4];
+#pragma unroll
+    for (int j = 0; j < kConsumerWarps / 4; ++j) v[j] = __ldcg(w + sub * (kConsumerWarps / 4) + j);
+#pragma unroll
+    for (int j = 0; j < kConsumerWarps / 4; ++j) s = (((s + v[j].x) + v[j].y) + v[j].z) + v[j].w;
+  }
   return s;
 }
 
@@ -227,12 +284,162 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
   }
 }
 
+
 __device__ __forceinline__ int32_t checked_phys(const DistArgs& a, int32_t p) {
   if (p < 0 || p >= a.num_blocks) {
     set_status(a.status, MEMSHARE_ERR_CORRUPTION);
     return 0;
   }
   return p;
+}
+
+// ------------------------------------------------------------------------------ planning
+// Items: targets that share their first (smallest-logical) source block are near-copies of one
+// earlier step at the same block offset (redundant steps repeat an earlier
+// one), so they share most of their sources. Targets are sorted by (first source, index) in
+// shared memory; each run of <= kAnchors consecutive targets with the same key whose pairs fit
+// in kItemPairs becomes one item, otherwise each target becomes its own item(s) of <= 64 pairs.
+// Larger inputs (T > kPlanSortCap) use one-target items. One CTA, fully parallel, deterministic.
+constexpr int kPlanSortCap = 8192;
+
+__device__ __forceinline__ int64_t pair_lo(const DistArgs& a, int64_t t) { return __ldcg(a.target_off + t); }
+
+__device__ __forceinline__ int64_t pairs_of(const DistArgs& a, int64_t t, int64_t P) {
+  const int64_t lo = __ldcg(a.target_off + t);
+  int64_t hi = __ldcg(a.target_off + t + 1);
+  if (hi > P) hi = P;
+  return hi > lo ? hi - lo : 0;
+}
+
+__device__ __forceinline__ int32_t solo_items(int64_t np) { return (int32_t)((np + kItemPairs - 1) / kItemPairs); }
+
+__device__ void write_solo(const DistArgs& a, int64_t t, int64_t P, int64_t at) {
+  const int64_t lo = pair_lo(a, t);
+  const int64_t hi = lo + pairs_of(a, t, P);
+  for (int64_t c0 = lo; c0 < hi; c0 += kItemPairs, ++at) {
+    ItemRec r;
+    r.na = 1; r.tgt[0] = (int32_t)t; r.lo[0] = (int32_t)c0;
+    r.hi[0] = (int32_t)(c0 + kItemPairs < hi ? c0 + kItemPairs : hi);
+    a.ws.items[at] = r;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(DistArgs a) {
+  extern __shared__ unsigned long long keys[];           // [pow2(T)] when T <= kPlanSortCap
+  __shared__ int64_t sh[kPlanThreads / 32 + 1];
+  const int tid = threadIdx.x;
+  const int64_t T = clamp_count(a.num_targets, a.target_cap);
+  const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
+  if (T > a.plan_sort_cap) {                               // one-target items
+    for (int64_t t = tid; t < T; t += kPlanThreads) a.ws.cnt[t] = solo_items(pairs_of(a, t, P));
+    __syncthreads();
+    cta_scan_counts<kPlanThreads>(a.ws.cnt, a.ws.item_off, T, sh);
+    __syncthreads();
+    for (int64_t t = tid; t < T; t += kPlanThreads) write_solo(a, t, P, __ldcg(a.ws.item_off + t));
+    if (tid == 0) *a.ws.n_items = __ldcg(a.ws.item_off + T);
+    return;
+  }
+  int np2 = 1;
+  while (np2 < T) np2 <<= 1;
+  for (int q = tid; q < np2; q += kPlanThreads) {
+    unsigned long long k = ~0ull;
+    if (q < T) {
+      const int64_t n = pairs_of(a, q, P);
+      const uint32_t first = n > 0 ? (uint32_t)checked_phys(a, a.pairs[pair_lo(a, q)].source_phys) : 0xFFFFFFFFu;
+      k = ((unsigned long long)first << 32) | (uint32_t)q;
+    }
+    keys[q] = k;
+  }
+  __syncthreads();
+  for (int k = 2; k <= np2; k <<= 1)                      // bitonic sort, ascending
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < np2; i += kPlanThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long x = keys[i], y = keys[ixj];
+          if (((i & k) == 0) ? (x > y) : (x < y)) { keys[i] = y; keys[ixj] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  // run starts: position q whose rank within its key group is a multiple of kAnchors
+  for (int q = tid; q < T; q += kPlanThreads) {
+    const unsigned long long kq = keys[q] >> 32;
+    int lo = 0, hi = q;                                    // first position with the same key
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((keys[mid] >> 32) < kq) lo = mid + 1; else hi = mid; }
+    const int gstart = lo;
+    int32_t items = 0;
+    if ((q - gstart) % kAnchors == 0 && kq != 0xFFFFFFFFull) {
+      int glen = 1;
+      while (glen < kAnchors && q + glen < T && (keys[q + glen] >> 32) == kq) ++glen;
+      int64_t sum = 0;
+      for (int m = 0; m < glen; ++m) sum += pairs_of(a, (int64_t)(keys[q + m] & 0xFFFFFFFFu), P);
+      if (sum <= kItemPairs) items = 1;
+      else for (int m = 0; m < glen; ++m) items += solo_items(pairs_of(a, (int64_t)(keys[q + m] & 0xFFFFFFFFu), P));
+    }
+    a.ws.cnt[q] = items;
+  }
+  __syncthreads();
+  cta_scan_counts<kPlanThreads>(a.ws.cnt, a.ws.item_off, T, sh);
+  __syncthreads();
+  for (int q = tid; q < T; q += kPlanThreads) {
+    if (__ldcg(a.ws.cnt + q) == 0) continue;
+    const unsigned long long kq = keys[q] >> 32;
+    int glen = 1;
+    while (glen < kAnchors && q + glen < T && (keys[q + glen] >> 32) == kq) ++glen;
+    int64_t at = __ldcg(a.ws.item_off + q);
+    int64_t sum = 0;
+    for (int m = 0; m < glen; ++m) sum += pairs_of(a, (int64_t)(keys[q + m] & 0xFFFFFFFFu), P);
+    if (sum <= kItemPairs) {
+      ItemRec r;
+      r.na = glen;
+      for (int m = 0; m < glen; ++m) {
+        const int64_t t = (int64_t)(keys[q + m] & 0xFFFFFFFFu);
+        r.tgt[m] = (int32_t)t; r.lo[m] = (int32_t)pair_lo(a, t); r.hi[m] = (int32_t)(pair_lo(a, t) + pairs_of(a, t, P));
+      }
+      a.ws.items[at] = r;
+    } else {
+      for (int m = 0; m < glen; ++m) {
+        const int64_t t = (int64_t)(keys[q + m] & 0xFFFFFFFFu);
+        write_solo(a, t, P, at);
+        at += solo_items(pairs_of(a, t, P));
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *a.ws.n_items = __ldcg(a.ws.item_off + T);
+}
+
+// ------------------------------------------------------------------------------ streaming
+#if MS_ANCHOR_FP32
+using AnchorT = float2[kR * 4];
+#else
+using AnchorT = uint4[kR];
+#endif
+
+template <int K>
+__device__ __forceinline__ float dist2_anchor(const AnchorT (&A)[kAnchors], const uint4 (&x)[kR]) {
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+  const float2 neg1 = make_float2(-1.f, -1.f);
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+#if MS_ANCHOR_FP32
+    const float2 t0 = A[K][4 * r + 0], t1 = A[K][4 * r + 1], t2 = A[K][4 * r + 2], t3 = A[K][4 * r + 3];
+#else
+    const float2 t0 = bf2_to_f2(A[K][r].x), t1 = bf2_to_f2(A[K][r].y), t2 = bf2_to_f2(A[K][r].z),
+                 t3 = bf2_to_f2(A[K][r].w);
+#endif
+    // d = t - s exactly rounded (fma with -1; the anchor is the register operand), acc += d*d
+    const float2 d0 = __ffma2_rn(bf2_to_f2(x[r].x), neg1, t0);
+    const float2 d1 = __ffma2_rn(bf2_to_f2(x[r].y), neg1, t1);
+    const float2 d2 = __ffma2_rn(bf2_to_f2(x[r].z), neg1, t2);
+    const float2 d3 = __ffma2_rn(bf2_to_f2(x[r].w), neg1, t3);
+    acc0 = __ffma2_rn(d0, d0, acc0);
+    acc1 = __ffma2_rn(d1, d1, acc1);
+    acc0 = __ffma2_rn(d2, d2, acc0);
+    acc1 = __ffma2_rn(d3, d3, acc1);
+  }
+  return (acc0.x + acc0.y) + (acc1.x + acc1.y);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
@@ -251,134 +458,206 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------------ producer warp
-    // All 32 lanes stage the item's source ids into smem (one coalesced round trip instead of
-    // a dependent global load per copy) and lane 0 fetches the next ticket while the current
-    // item's copies are issued, so the ring never waits on metadata latency.
-    const int64_t T = clamp_count(a.num_targets, a.target_cap);
-    const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
-    const int64_t total = T * a.n_chunks;
+    // with one anchor an item is a target (no planning launch); otherwise plan_kernel's items
+    const int64_t I = kAnchors == 1 ? clamp_count(a.num_targets, a.target_cap) : __ldcg(a.ws.n_items);
+    const int64_t Pn = clamp_count(a.num_pairs, a.pair_cap);
+    const int64_t total = I * a.n_chunks;
     int stage = 0;
     uint32_t ph = 0;
-    auto push = [&](const Meta& m, const uint8_t* src) {
-      mbar_wait(&sm.empty[stage], ph ^ 1u);
-      sm.meta[stage] = m;
-      if (src != nullptr) {
-        mbar_expect_tx(&sm.full[stage], (uint32_t)m.bytes);
-        for (int off = 0; off < m.bytes; off += kCopyPiece) {
-          const int nb = (m.bytes - off) < kCopyPiece ? (m.bytes - off) : kCopyPiece;
-          bulk_g2s(sm.ring[stage] + off, src + off, (uint32_t)nb, &sm.full[stage]);
-        }
-      } else {
-        mbar_arrive(&sm.full[stage]);
-      }
-      if (++stage == kStages) { stage = 0; ph ^= 1u; }
-    };
-    int64_t item = 0;
-    if (lane == 0) item = (int64_t)atomicAdd(a.ws.ticket, 1u);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    while (item < total) {
+    ProdSmem& ps = sm.prod;
+    int64_t unit = 0;
+    if (lane == 0) unit = (int64_t)atomicAdd(a.ws.ticket, 1u);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    while (unit < total) {
       int64_t next = 0;
-      if (lane == 0) next = (int64_t)atomicAdd(a.ws.ticket, 1u);   // consumed at the end of the item
-      const int64_t lc = item / T, t = item - lc * T;
-      const int64_t p0 = __ldcg(a.target_off + t);
-      int64_t p1 = __ldcg(a.target_off + t + 1);
-      if (p1 > P) p1 = P;
-      const int64_t np = p1 - p0;
-      for (int64_t q = lane; q < np && q < kMaxStagedPairs; q += 32)
-        sm.src_phys[q] = checked_phys(a, a.pairs[p0 + q].source_phys);
-      const int32_t tphys = np > 0 ? checked_phys(a, a.pairs[p0].target_phys) : 0;
+      if (lane == 0) next = (int64_t)atomicAdd(a.ws.ticket, 1u);   // consumed at the end of the unit
+      const int64_t lc = unit / I, it = unit - lc * I;
+      ItemRec rec0;
+      if (kAnchors == 1) {
+        rec0.na = 1; rec0.tgt[0] = (int32_t)it;
+        const int64_t lo = __ldcg(a.target_off + it);
+        int64_t hi = __ldcg(a.target_off + it + 1);
+        if (hi > Pn) hi = Pn;
+        rec0.lo[0] = (int32_t)lo; rec0.hi[0] = (int32_t)(hi > lo ? hi : lo);
+      } else {
+        rec0 = a.ws.items[it];
+      }
+      // a target with more than kItemPairs pairs is processed in chunks (anchor reloaded per chunk)
+      for (int32_t c0 = rec0.lo[0]; c0 < rec0.hi[0] || (c0 == rec0.lo[0] && rec0.na > 1); c0 += kItemPairs) {
+      ItemRec rec = rec0;
+      if (rec0.na == 1) { rec.lo[0] = c0; rec.hi[0] = (c0 + kItemPairs < rec0.hi[0]) ? c0 + kItemPairs : rec0.hi[0]; }
+      // stage the item's pairs: entry e -> (anchor, pair, source phys)
+      int32_t off[kAnchors + 1];
+      off[0] = 0;
+#pragma unroll
+      for (int i = 0; i < kAnchors; ++i) off[i + 1] = off[i] + (i < rec.na ? rec.hi[i] - rec.lo[i] : 0);
+      const int32_t ne = off[kAnchors];
+      if (lane < rec.na) ps.aphys[lane] = checked_phys(a, a.pairs[rec.lo[lane]].target_phys);
+      for (int32_t e = lane; e < ne; e += 32) {
+        int i = 0;
+        while (i + 1 < rec.na && e >= off[i + 1]) ++i;
+        const int32_t p = rec.lo[i] + (e - off[i]);
+        ps.ent_pair[e] = p;
+        ps.ent_anc[e] = (int8_t)i;
+        ps.ent_phys[e] = checked_phys(a, a.pairs[p].source_phys);
+      }
+      __syncwarp();
+      // classify: source is an anchor block -> evaluated at the later anchor's stage;
+      // otherwise streamed once per distinct physical block (first occurrence streams).
+      for (int32_t e = lane; e < ne; e += 32) {
+        const int32_t ph_e = ps.ent_phys[e];
+        int kind = -1;
+        for (int j = 0; j < rec.na; ++j)
+          if (ps.aphys[j] == ph_e) { kind = j; break; }
+        if (kind < 0) {
+          for (int32_t e2 = 0; e2 < e; ++e2)
+            if (ps.ent_phys[e2] == ph_e) {
+              bool e2_anchor = false;
+              for (int j = 0; j < rec.na; ++j) e2_anchor |= (ps.aphys[j] == ph_e);
+              if (!e2_anchor) { kind = -2; break; }
+            }
+        }
+        ps.ent_kind[e] = (int8_t)kind;
+      }
       __syncwarp();
       if (lane == 0) {
-        Meta m{};
-        m.target = t;
-        if (np <= 0) {
-          m.pair = -1; m.flags = F_ITEM_END | F_SKIP;
-          push(m, nullptr);
-        } else {
-          const int32_t l0 = (int32_t)lc * a.lpi;
-          const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
-          for (int32_t l = l0; l < l1; ++l) {
-            for (int32_t kv = 0; kv < 2; ++kv) {
-              const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
-              for (int32_t sub = 0; sub < a.n_sub; ++sub) {
-                const int32_t off = sub * a.sub_bytes;
-                const int32_t bytes = (a.slice_bytes - off) < a.sub_bytes ? (a.slice_bytes - off) : a.sub_bytes;
-                m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes;
-                m.pair = -1; m.flags = F_TARGET;
-                push(m, base + (int64_t)tphys * a.block_stride_b + off);
-                for (int64_t q = 0; q < np; ++q) {
-                  const int32_t sphys = q < kMaxStagedPairs ? sm.src_phys[q]
-                                                            : checked_phys(a, a.pairs[p0 + q].source_phys);
-                  m.pair = p0 + q;
-                  m.flags = (l == l1 - 1 && kv == 1 && sub == a.n_sub - 1 && q == np - 1) ? F_ITEM_END : 0;
-                  push(m, base + (int64_t)sphys * a.block_stride_b + off);
-                }
+        // stage templates, built once per unit: anchors first (each carrying the anchor-anchor
+        // pairs completed by its arrival), then one stage per distinct streamed source
+        int32_t nt = 0;
+        auto open_tpl = [&](int32_t phys, int32_t anchor) {
+          StageTpl& t = ps.tpl[nt++];
+          t.phys = phys; t.anchor = anchor; t.nent = 0;
+          return &t;
+        };
+        for (int j = 0; j < rec.na; ++j) {
+          StageTpl* t = open_tpl(ps.aphys[j], j);
+          for (int32_t e = 0; e < ne; ++e) {
+            const int k = ps.ent_kind[e];
+            if (k < 0) continue;
+            const int i = ps.ent_anc[e];
+            if ((i > k ? i : k) != j) continue;
+            if (t->nent == kMetaEnt) t = open_tpl(ps.aphys[j], j);   // overflow: reload the anchor
+            t->pair[t->nent] = ps.ent_pair[e];
+            t->anc[t->nent] = (int8_t)(i > k ? k : i);
+            t->nent += 1;
+          }
+        }
+        for (int32_t e = 0; e < ne; ++e) {
+          if (ps.ent_kind[e] != -1) continue;
+          const int32_t phe = ps.ent_phys[e];
+          StageTpl* t = open_tpl(phe, -1);
+          for (int32_t e2 = e; e2 < ne; ++e2) {
+            if (ps.ent_kind[e2] >= 0 || ps.ent_phys[e2] != phe) continue;
+            if (t->nent == kMetaEnt) t = open_tpl(phe, -1);
+            t->pair[t->nent] = ps.ent_pair[e2];
+            t->anc[t->nent] = ps.ent_anc[e2];
+            t->nent += 1;
+          }
+        }
+        const int32_t l0 = (int32_t)lc * a.lpi;
+        const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
+        for (int32_t l = l0; l < l1; ++l) {
+          for (int32_t kv = 0; kv < 2; ++kv) {
+            const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
+            for (int32_t sub = 0; sub < a.n_sub; ++sub) {
+              const int32_t boff = sub * a.sub_bytes;
+              const int32_t bytes = (a.slice_bytes - boff) < a.sub_bytes ? (a.slice_bytes - boff) : a.sub_bytes;
+              for (int32_t ti = 0; ti < nt; ++ti) {
+                const StageTpl& t = ps.tpl[ti];
+                mbar_wait(&sm.empty[stage], ph ^ 1u);
+                Meta& m = sm.meta[stage];
+#pragma unroll
+                for (int e = 0; e < kMetaEnt; ++e) { m.pair[e] = t.pair[e]; m.anc[e] = t.anc[e]; }
+                m.nent = t.nent; m.anchor = t.anchor;
+                m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes; m.flags = 0;
+                mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
+                bulk_g2s(sm.ring[stage], base + (int64_t)t.phys * a.block_stride_b + boff, (uint32_t)bytes,
+                         &sm.full[stage]);
+                if (++stage == kStages) { stage = 0; ph ^= 1u; }
               }
             }
           }
         }
       }
       __syncwarp();
-      item = __shfl_sync(0xffffffffu, next, 0);
+      if (rec0.na > 1) break;
+      }
+      __syncwarp();
+      unit = __shfl_sync(0xffffffffu, next, 0);
     }
     if (lane == 0) {
-      Meta stop{};
-      stop.flags = F_STOP;
-      push(stop, nullptr);
+      mbar_wait(&sm.empty[stage], ph ^ 1u);
+      sm.meta[stage].flags = F_STOP;
+      sm.meta[stage].nent = 0;
+      sm.meta[stage].anchor = -1;
+      mbar_arrive(&sm.full[stage]);
     }
     return;
   }
 
   // -------------------------------------------------------------------- consumer warps
-  float2 tv[kR * 4];
+  AnchorT A[kAnchors];
   int stage = 0;
   uint32_t ph = 0;
   for (;;) {
     mbar_wait(&sm.full[stage], ph);
-    const Meta m = sm.meta[stage];
-    if (m.flags & F_STOP) break;
-    if (!(m.flags & F_SKIP) && !MS_DIAG_NO_COMPUTE) {
-      const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
-      const int nchunk = m.bytes >> 4;
-      if (m.flags & F_TARGET) {
+    const Meta& mr = sm.meta[stage];
+    const int flags = mr.flags;
+    if (flags & F_STOP) break;
+    const int anchor = mr.anchor, nent = mr.nent, layer = mr.layer, kv = mr.kv, sub = mr.sub;
+    uint32_t ent[kMetaEnt];                                  // pair id << 2 | anchor slot
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const int c = tid + r * kConsumers;
-          uint4 x = make_uint4(0u, 0u, 0u, 0u);
-          if (c < nchunk) x = src[c];
-          tv[4 * r + 0] = bf2_to_f2(x.x);
-          tv[4 * r + 1] = bf2_to_f2(x.y);
-          tv[4 * r + 2] = bf2_to_f2(x.z);
-          tv[4 * r + 3] = bf2_to_f2(x.w);
-        }
-      } else {
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-        const float2 neg1 = make_float2(-1.f, -1.f);
+    for (int e = 0; e < kMetaEnt; ++e) ent[e] = ((uint32_t)mr.pair[e] << 2) | ((uint32_t)mr.anc[e] & 3u);
+    const int nchunk = mr.bytes >> 4;
+    const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
+    uint4 x[kR];
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const int c = tid + r * kConsumers;
-          if (c < nchunk) {
-            const uint4 x = src[c];
-            // d = t - s exactly rounded (fma with -1), acc += d*d; packed f32x2 (FFMA2)
-            const float2 d0 = __ffma2_rn(bf2_to_f2(x.x), neg1, tv[4 * r + 0]);
-            const float2 d1 = __ffma2_rn(bf2_to_f2(x.y), neg1, tv[4 * r + 1]);
-            const float2 d2 = __ffma2_rn(bf2_to_f2(x.z), neg1, tv[4 * r + 2]);
-            const float2 d3 = __ffma2_rn(bf2_to_f2(x.w), neg1, tv[4 * r + 3]);
-            acc0 = __ffma2_rn(d0, d0, acc0);
-            acc1 = __ffma2_rn(d1, d1, acc1);
-            acc0 = __ffma2_rn(d2, d2, acc0);
-            acc1 = __ffma2_rn(d3, d3, acc1);
-          }
-        }
-        float s = (acc0.x + acc0.y) + (acc1.x + acc1.y);
-        s = warp_sum(s);
-        if (lane == 0)
-          a.ws.wpart[(((m.pair * a.N + m.layer) * 2 + m.kv) * a.n_sub + m.sub) * kConsumerWarps + warp] = s;
-      }
+    for (int r = 0; r < kR; ++r) {
+      const int c = tid + r * kConsumers;
+      x[r] = (!MS_DIAG_NO_COMPUTE && c < nchunk) ? src[c] : make_uint4(0u, 0u, 0u, 0u);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);            // stage free: data is in registers
     if (++stage == kStages) { stage = 0; ph ^= 1u; }
+    if (MS_DIAG_NO_COMPUTE) continue;
+    if (anchor >= 0) {
+#pragma unroll
+      for (int j = 0; j < kAnchors; ++j)
+        if (j == anchor) {
+#pragma unroll
+          for (int r = 0; r < kR; ++r) {
+#if MS_ANCHOR_FP32
+            A[j][4 * r + 0] = bf2_to_f2(x[r].x);
+            A[j][4 * r + 1] = bf2_to_f2(x[r].y);
+            A[j][4 * r + 2] = bf2_to_f2(x[r].z);
+            A[j][4 * r + 3] = bf2_to_f2(x[r].w);
+#else
+            A[j][r] = x[r];
+#endif
+          }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < kMetaEnt; ++e) {
+      if (e >= nent) break;
+      float sacc;
+      switch (ent[e] & 3u) {                                 // warp-uniform
+        case 0: sacc = dist2_anchor<0>(A, x); break;
+#if MS_ANCHORS > 1
+        case 1: sacc = dist2_anchor<1>(A, x); break;
+#endif
+#if MS_ANCHORS > 2
+        case 2: sacc = dist2_anchor<2>(A, x); break;
+#endif
+#if MS_ANCHORS > 3
+        case 3: sacc = dist2_anchor<3>(A, x); break;
+#endif
+        default: sacc = 0.f;
+      }
+      sacc = warp_sum(sacc);
+      if (lane == 0)
+        a.ws.wpart[((((int64_t)(ent[e] >> 2) * a.N + layer) * 2 + kv) * a.n_sub + sub) * kConsumerWarps + warp] = sacc;
+    }
   }
 }
 
@@ -392,6 +671,7 @@ __global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int fr
     finalize_target(a, t, terms, threadIdx.x, from_partial != 0, [] { __syncthreads(); });
 }
 
+
 }  // namespace
 }  // namespace ms
 
@@ -401,12 +681,12 @@ static int32_t n_sub_of(int64_t slice_bytes) {
   return (int32_t)((slice_bytes + kStageBytes - 1) / kStageBytes);
 }
 
-extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* dims, int64_t pair_cap,
-                                                         int64_t target_cap) {
-  if (!dims || pair_cap < 0 || target_cap < 0 || dims->num_layers < 1) return 0;
+extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* dims, int32_t num_blocks,
+                                                         int64_t pair_cap, int64_t target_cap) {
+  if (!dims || pair_cap < 0 || target_cap < 0 || num_blocks < 0 || dims->num_layers < 1) return 0;
   const int64_t slice = (int64_t)dims->block_size * dims->num_kv_heads_local * dims->head_dim * 2;
   Ws w{nullptr, 0};
-  dist_layout(w, dims->num_layers, n_sub_of(slice), pair_cap, target_cap);
+  dist_layout(w, dims->num_layers, n_sub_of(slice), num_blocks, pair_cap, target_cap);
   return w.size();
 }
 
@@ -420,7 +700,8 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   if (!dims || !pairs || !target_off || !num_pairs || !num_targets || !workspace || !device_status)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (mode < MEMSHARE_DIST_FULL || mode > MEMSHARE_DIST_FINALIZE) return MEMSHARE_ERR_INVALID_ARGUMENT;
-  if (pair_cap < 0 || target_cap < 0) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (pair_cap < 0 || pair_cap > ((int64_t)1 << 30) || target_cap < 0 || target_cap > (int64_t)INT32_MAX)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
   const memshare_dims dm = *dims;
   if (dm.num_layers < 1 || dm.num_layers > 256 || dm.num_kv_heads_local < 1 || dm.num_kv_heads_global < 1 ||
       dm.num_kv_heads_local > dm.num_kv_heads_global || dm.head_dim < 8 || dm.head_dim % 8 != 0 || dm.block_size < 1)
@@ -430,13 +711,15 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   if (mode != MEMSHARE_DIST_FULL && !partial_sq) return MEMSHARE_ERR_INVALID_ARGUMENT;
   const int64_t slice_bytes = (int64_t)dm.block_size * dm.num_kv_heads_local * dm.head_dim * 2;
   if (slice_bytes > (int64_t)INT32_MAX / 2) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  int32_t num_blocks = 0;
   if (mode != MEMSHARE_DIST_FINALIZE) {
     if (!pool || !pool->k || !pool->v || pool->num_blocks < 0) return MEMSHARE_ERR_INVALID_ARGUMENT;
     if (!aligned16(pool->k) || !aligned16(pool->v) || (pool->layer_stride * 2) % 16 != 0 ||
         (pool->block_stride * 2) % 16 != 0 || pool->layer_stride < 0 || pool->block_stride < 0)
       return MEMSHARE_ERR_INVALID_ARGUMENT;
+    num_blocks = pool->num_blocks;
   }
-  if (workspace_bytes < memshare_block_distance_workspace_size(dims, pair_cap, target_cap))
+  if (workspace_bytes < memshare_block_distance_workspace_size(dims, num_blocks, pair_cap, target_cap))
     return MEMSHARE_ERR_INVALID_ARGUMENT;
 
   DistArgs a{};
@@ -445,8 +728,8 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
     a.vbase = static_cast<const uint8_t*>(pool->v);
     a.layer_stride_b = pool->layer_stride * 2;
     a.block_stride_b = pool->block_stride * 2;
-    a.num_blocks = pool->num_blocks;
   }
+  a.num_blocks = num_blocks;
   a.N = dm.num_layers; a.d = dm.block_size; a.h_global = dm.num_kv_heads_global;
   a.slice_bytes = (int32_t)slice_bytes;
   a.n_sub = n_sub_of(slice_bytes);
@@ -464,7 +747,12 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   a.pair_cap = pair_cap; a.target_cap = target_cap; a.mode = mode; a.partial_sq = partial_sq; a.tau_b = tau_b;
   a.distance = distance; a.under = under; a.decisions = decisions; a.status = device_status;
   Ws w{static_cast<char*>(workspace), 0};
-  a.ws = dist_layout(w, a.N, a.n_sub, pair_cap, target_cap);
+  a.ws = dist_layout(w, a.N, a.n_sub, num_blocks, pair_cap, target_cap);
+  {
+    int64_t np2 = 1;
+    while (np2 < target_cap && np2 < kPlanSortCap) np2 <<= 1;
+    a.plan_sort_cap = (int32_t)np2;
+  }
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t tc = target_cap < 1 ? 1 : target_cap;
@@ -476,11 +764,16 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(distance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DistSmem)) !=
-        cudaSuccess)
+            cudaSuccess ||
+        cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kPlanSortCap * sizeof(unsigned long long))) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
     attr_set = true;
   }
   if (cudaMemsetAsync(a.ws.ticket, 0, sizeof(unsigned int), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  int64_t plan_np2 = 1;
+  while (plan_np2 < target_cap && plan_np2 < kPlanSortCap) plan_np2 <<= 1;
+  if (kAnchors > 1) plan_kernel<<<1, kPlanThreads, (size_t)plan_np2 * sizeof(unsigned long long), st>>>(a);
   distance_kernel<<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
   finalize_kernel<<<fin_grid, kConsumers, 0, st>>>(a, 0);
   return launch_status();

@@ -99,7 +99,7 @@ class MemSharePath:
         self.decisions = e(caps.target * 32, torch.uint8)
         ws = max(L.segment_steps_workspace_size(self.num_tokens, self.num_seqs, caps.step),
                  L.step_candidates_workspace_size(self.num_tokens, self.num_seqs, caps.step, caps.match),
-                 L.block_distance_workspace_size(self.dims, caps.pair, caps.target),
+                 L.block_distance_workspace_size(self.dims, self.num_blocks, caps.pair, caps.target),
                  L.remap_workspace_size(self.num_blocks, caps.target))
         self.workspace = e(ws, torch.uint8)
 

@@ -57,7 +57,7 @@ def test_workspace_sizes_are_host_only(lib):
     assert lib.segment_steps_workspace_size(1000, 10, 100) > 0
     assert lib.step_candidates_workspace_size(1000, 2, 100, 50) > lib.step_candidates_workspace_size(10, 2, 100, 50)
     d = lib.Dims(64, 8, 8, 128, 16)
-    assert lib.block_distance_workspace_size(d, 100, 10) >= 100 * 64 * 2 * 8 * 4
+    assert lib.block_distance_workspace_size(d, 50, 100, 10) >= 100 * 64 * 2 * 8 * 4
     assert lib.remap_workspace_size(100, 10) > 0
 
 

@@ -190,7 +190,7 @@ def test_distance_properties_on_gpu():
     dist = torch.empty(7, dtype=torch.float32, device=dev)
     under = torch.empty(7, dtype=torch.uint8, device=dev)
     dec = torch.empty(7 * 32, dtype=torch.uint8, device=dev)
-    ws = torch.empty(L.block_distance_workspace_size(dims, 7, 7), dtype=torch.uint8, device=dev)
+    ws = torch.empty(L.block_distance_workspace_size(dims, nb, 7, 7), dtype=torch.uint8, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     assert L.block_distance(pool, dims, pairs, toff, npairs, ntg, 7, 7, L.DIST_FULL, None, 0.3, dist, under, dec, ws,
                             status) == 0
