@@ -29,9 +29,9 @@ namespace {
 constexpr int kNT = 256;          // encode / fill
 constexpr int kNT1 = 1024;        // stage1 (one CTA per current step: widest history stream)
 constexpr int kNW1 = kNT1 / 32;
-constexpr int kUnroll = 4;
+constexpr int kTokRun = 16;      // tokens per thread-run in the stage-1 history stream
 constexpr int kNW = kNT / 32;
-constexpr int kSmemSlots = 4096;       // smem hash table (steps with <= 2048 content tokens)
+constexpr int kSmemSlots = 8192;       // smem hash table (steps with <= 2048 content tokens, load <= 0.25)
 constexpr int kCandCap = 1024;         // survivors held per current step
 constexpr int kChunk = kCandCap / 2;   // history steps per selection chunk
 constexpr int kMaxTgt = 4096;          // full blocks per step handled by the fill kernel
@@ -52,8 +52,7 @@ struct CandWs {
   double* stash_cos;     // [match_cap]
   int32_t* stash_j;
   int32_t* tok_step;     // [num_tokens] global step of each token inside a finished step
-  int32_t* gkeys;        // [4*num_tokens]
-  int32_t* gcnts;
+  int2* gtab;            // [4*num_tokens] {key, count} global tables of oversize steps
 };
 
 CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_cap) {
@@ -72,8 +71,7 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   c.stash_cos = w.take<double>(match_cap + 1);
   c.stash_j = w.take<int32_t>(match_cap + 1);
   c.tok_step = w.take<int32_t>(num_tokens + 1);
-  c.gkeys = w.take<int32_t>(4 * num_tokens + 1);
-  c.gcnts = w.take<int32_t>(4 * num_tokens + 1);
+  c.gtab = w.take<int2>(4 * num_tokens + 1);
   return c;
 }
 
@@ -116,51 +114,50 @@ __device__ __forceinline__ int64_t total_steps(const CandArgs& a) {
   return g < a.step_cap ? g : a.step_cap;
 }
 
-__device__ __forceinline__ uint32_t hash_slot(int32_t tok, uint32_t mask) {
-  return ((uint32_t)tok * 0x9E3779B1u) & mask;
+// multiplicative hash, top bits (the well-mixed ones); `shift` = 32 - log2(capacity)
+__device__ __forceinline__ uint32_t hash_slot(int32_t tok, uint32_t shift) {
+  return ((uint32_t)tok * 0x9E3779B1u) >> shift;
 }
 
 __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) { return x <= 1 ? 1u : 1u << (32 - __clz(x - 1)); }
 __device__ __forceinline__ uint32_t pow2_floor(uint32_t x) { return 1u << (31 - __clz(x)); }
 
-// Count table of one step: keys/cnts live in smem (small steps) or in the step's private
-// region of the global workspace (4 slots per token of the step).
+// Count table of one step, {key, count} pairs with open addressing: in smem (steps with <= 2048
+// content tokens, load factor <= 0.25) or in the step's private region of the global workspace
+// (4 slots per token of the step, load factor <= 0.5).
 struct Table {
-  int32_t* keys;
-  int32_t* cnts;
+  int2* slots;
   uint32_t mask;
+  uint32_t shift;
   bool global;
 };
 
-__device__ Table build_table(const CandArgs& a, int32_t* s_keys, int32_t* s_cnts, const int32_t* t, int64_t tok_base,
-                             int32_t start, int32_t end, int32_t nbag) {
+__device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, int64_t tok_base, int32_t start,
+                             int32_t end, int32_t nbag) {
   Table tb;
   uint32_t cap;
-  if (nbag <= kSmemSlots / 2) {
-    cap = pow2_ceil(2u * (uint32_t)(nbag > 32 ? nbag : 32));
-    tb.keys = s_keys;
-    tb.cnts = s_cnts;
+  if (nbag <= kSmemSlots / 4) {
+    cap = pow2_ceil(4u * (uint32_t)(nbag > 32 ? nbag : 32));
+    tb.slots = s_tab;
     tb.global = false;
   } else {
     cap = pow2_floor(4u * (uint32_t)(end - start));
-    tb.keys = a.ws.gkeys + 4 * (tok_base + start);
-    tb.cnts = a.ws.gcnts + 4 * (tok_base + start);
+    tb.slots = a.ws.gtab + 4 * (tok_base + start);
     tb.global = true;
   }
   tb.mask = cap - 1;
-  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
-    tb.keys[i] = kEmpty;
-    tb.cnts[i] = 0;
-  }
+  tb.shift = 32u - (31u - __clz(cap));
+  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) tb.slots[i] = make_int2(kEmpty, 0);
   __syncthreads();
   for (int32_t p = start + threadIdx.x; p < end; p += blockDim.x) {
     const int32_t tok = t[p];
     if (is_delim(tok, a.dl)) continue;
-    uint32_t slot = hash_slot(tok, tb.mask);
+    uint32_t slot = hash_slot(tok, tb.shift);
     for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
-      const int32_t prev = atomicCAS(tb.keys + slot, kEmpty, tok);
+      int* key = &tb.slots[slot].x;
+      const int32_t prev = atomicCAS(key, kEmpty, tok);
       if (prev == kEmpty || prev == tok) {
-        atomicAdd(tb.cnts + slot, 1);
+        atomicAdd(&tb.slots[slot].y, 1);
         break;
       }
       slot = (slot + 1) & tb.mask;
@@ -170,24 +167,26 @@ __device__ Table build_table(const CandArgs& a, int32_t* s_keys, int32_t* s_cnts
   return tb;
 }
 
-// smem-only probe (keys/cnts derived from the kernel's shared array -> LDS, not generic loads)
-__device__ __forceinline__ int32_t table_get_smem(const int32_t* keys, const int32_t* cnts, uint32_t mask, int32_t tok) {
-  uint32_t slot = hash_slot(tok, mask);
+// smem-only probe (the table pointer is derived from the kernel's shared array -> LDS.64)
+__device__ __forceinline__ int32_t table_get_smem(const int2* tab, uint32_t mask, uint32_t shift, int32_t tok) {
+  uint32_t slot = hash_slot(tok, shift);
+#pragma unroll 1
   for (uint32_t probe = 0; probe <= mask; ++probe) {
-    const int32_t k = keys[slot];
-    if (k == tok) return cnts[slot];
-    if (k == kEmpty) return 0;
+    const int2 e = tab[slot];
+    if (e.x == tok) return e.y;
+    if (e.x == kEmpty) return 0;
     slot = (slot + 1) & mask;
   }
   return 0;
 }
 
 __device__ __forceinline__ int32_t table_get(const Table& tb, int32_t tok) {
-  uint32_t slot = hash_slot(tok, tb.mask);
+  uint32_t slot = hash_slot(tok, tb.shift);
+#pragma unroll 1
   for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
-    const int32_t k = tb.global ? __ldcg(tb.keys + slot) : tb.keys[slot];
-    if (k == tok) return tb.global ? __ldcg(tb.cnts + slot) : tb.cnts[slot];
-    if (k == kEmpty) return 0;
+    const int2 e = tb.global ? __ldcg(tb.slots + slot) : tb.slots[slot];
+    if (e.x == tok) return e.y;
+    if (e.x == kEmpty) return 0;
     slot = (slot + 1) & tb.mask;
   }
   return 0;
@@ -203,8 +202,7 @@ __device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {
 }
 
 __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
-  __shared__ int32_t s_keys[kSmemSlots];
-  __shared__ int32_t s_cnts[kSmemSlots];
+  extern __shared__ int2 s_tab[];                         // [kSmemSlots]
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
   for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
@@ -214,9 +212,9 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
     for (int32_t p = a.step_start[g] + threadIdx.x; p < a.step_end[g]; p += kNT) a.ws.tok_step[tok_base + p] = (int32_t)g;
     int64_t n2 = 0;
     if (nbag > 0) {
-      const Table tb = build_table(a, s_keys, s_cnts, a.tokens + tok_base, tok_base, a.step_start[g], a.step_end[g], nbag);
+      const Table tb = build_table(a, s_tab, a.tokens + tok_base, tok_base, a.step_start[g], a.step_end[g], nbag);
       for (uint32_t i = threadIdx.x; i <= tb.mask; i += kNT) {
-        const int64_t c = tb.global ? __ldcg(tb.cnts + i) : tb.cnts[i];
+        const int64_t c = tb.global ? __ldcg(tb.slots + i).y : tb.slots[i].y;
         n2 += c * c;
       }
     }
@@ -372,6 +370,7 @@ __device__ __forceinline__ bool is_current(const CandArgs& a, int32_t s, int64_t
 // Tuning only (MEMSHARE_DEBUG_SKIP bit 3): per-CTA phase timestamps of stage1 (globaltimer ns).
 constexpr int kDbgSlots = 16;
 __device__ unsigned long long g_dbg_t[2048 * kDbgSlots];
+__device__ long long g_dbg_tok[2048 * 32];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -384,8 +383,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 struct SelSmem {
-  int32_t keys[kSmemSlots];
-  int32_t cnts[kSmemSlots];
+  int2 tab[kSmemSlots];
   double cs[kCandCap];
   int32_t js[kCandCap];
   int32_t jasc[kCandCap];
@@ -394,13 +392,54 @@ struct SelSmem {
   int32_t cum[kCandCap + 1];
   int32_t hst[kChunk];
   int32_t hen[kChunk];
-  unsigned long long dot[kChunk];
+  uint32_t dot_lo[kChunk];
+  uint32_t dot_hi[kChunk];
   int64_t sh[kNW1 + 1];
   int count;
   int overflow;
-  int64_t acc_t;
-  int64_t acc_p;
+  uint32_t acc_t;
+  uint32_t acc_p;
 };
+
+template <bool kGlobal>
+__device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, uint32_t shift, uint32_t* dot_lo,
+                                               uint32_t* dot_hi, const int32_t* hen, int32_t d0, int32_t dn,
+                                               const Delims& dl, const int32_t* __restrict__ t,
+                                               const int32_t* __restrict__ ts, int32_t lo, int32_t hi, int64_t gjb,
+                                               bool dbg_noprobe) {
+  const int32_t n = hi - lo;
+  const int32_t per = (n + kNT1 - 1) / kNT1;                // tokens per thread
+  int32_t p = lo + (int32_t)threadIdx.x * per;
+  const int32_t pe = (p + per < hi) ? p + per : hi;
+  if (p >= pe) return;
+  int32_t jl = (int32_t)(__ldg(ts + p) - gjb);
+  int32_t bound = hen[jl];
+  uint32_t acc = 0u;
+  int32_t nxt = __ldg(t + p);                               // software-pipelined token load
+#pragma unroll 1
+  for (; p < pe; ++p) {
+    const int32_t tok = nxt;
+    if (p + 1 < pe) nxt = __ldg(t + p + 1);
+    if (p >= bound) {
+      if (acc) { const uint32_t old = atomicAdd(dot_lo + jl, acc); if (old + acc < old) atomicAdd(dot_hi + jl, 1u); }
+      acc = 0u;
+      do { ++jl; bound = hen[jl]; } while (p >= bound);
+    }
+    if (tok == d0 || (dn > 1 && is_delim(tok, dl))) continue;
+    if (dbg_noprobe) { acc += (uint32_t)(tok & 1); continue; }
+    uint32_t slot = hash_slot(tok, shift);
+    int32_t c = 0;
+#pragma unroll 1
+    for (uint32_t probe = 0; probe <= mask; ++probe) {
+      const int2 e = kGlobal ? __ldcg(tab + slot) : tab[slot];
+      if (e.x == tok) { c = e.y; break; }
+      if (e.x == kEmpty) break;
+      slot = (slot + 1) & mask;
+    }
+    acc += (uint32_t)c;
+  }
+  if (acc) { const uint32_t old = atomicAdd(dot_lo + jl, acc); if (old + acc < old) atomicAdd(dot_hi + jl, 1u); }
+}
 
 __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -420,7 +459,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
     }
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t* t = a.tokens + tok_base;
-    const Table tb = build_table(a, sm.keys, sm.cnts, t, tok_base, a.step_start[g], a.step_end[g], nbag);
+    const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag);
     DBG_T(1);
     const double n2k = (double)a.ws.n2[g];
     if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
@@ -435,36 +474,31 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       for (int i = threadIdx.x; i < nj; i += kNT1) {
         sm.hst[i] = a.step_start[gfirst + jb + i];
         sm.hen[i] = a.step_end[gfirst + jb + i];
-        sm.dot[i] = 0ull;
+        sm.dot_lo[i] = 0u;
+        sm.dot_hi[i] = 0u;
       }
       __syncthreads();
+      if (jb == 0) DBG_T(10);
       const int32_t lo = sm.hst[0], hi = sm.hen[nj - 1];
       const int32_t* ts = a.ws.tok_step + tok_base;
       const int64_t gjb = gfirst + jb;
-      for (int32_t base = lo + w * 32; base < hi && !(a.dbg_skip & 1); base += kNT1 * kUnroll) {
-        int32_t tok[kUnroll], js[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {       // issue all loads first (ILP)
-          const int32_t p = base + u * kNT1 + lane;
-          tok[u] = p < hi ? t[p] : a.dl.id[0];
-          js[u] = p < hi ? ts[p] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int32_t jl = js[u] < 0 ? -1 : (int32_t)(js[u] - gjb);
-          const bool valid = jl >= 0 && jl < nj && !is_delim(tok[u], a.dl);
-          const unsigned c = !valid ? 0u : (unsigned)(tb.global ? table_get(tb, tok[u]) : table_get_smem(sm.keys, sm.cnts, tb.mask, tok[u]));
-          // warp-aggregated accumulation: lanes of the same history step add once
-          const unsigned grp = __match_any_sync(0xffffffffu, jl);
-          const unsigned sum = __reduce_add_sync(grp, c);
-          if (sum != 0u && lane == __ffs(grp) - 1) atomicAdd(&sm.dot[jl], (unsigned long long)sum);
-        }
+      // each thread takes a contiguous run of tokens, walks the step boundaries in smem and adds
+      // its partial dot once per step it touches. A rolled loop on purpose: this code runs once
+      // per launch, so instruction-fetch misses of an unrolled body cost more than the loads.
+      if (!(a.dbg_skip & 1)) {
+        if (tb.global)
+          stream_history<true>(tb.slots, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, a.dl.id[0], a.dl.n, a.dl, t,
+                               ts, lo, hi, gjb, (a.dbg_skip & 16) != 0);
+        else
+          stream_history<false>(sm.tab, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, a.dl.id[0], a.dl.n, a.dl, t,
+                                ts, lo, hi, gjb, (a.dbg_skip & 16) != 0);
       }
       __syncthreads();
+      if (jb == 0) DBG_T(11);
       for (int i = threadIdx.x; i < nj; i += kNT1) {
         const int64_t gj = gfirst + jb + i;
         if (a.step_nbag[gj] == 0) continue;                // void history step (reading R5)
-        const int64_t dot = (int64_t)sm.dot[i];
+        const int64_t dot = (int64_t)(((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i]);
         // sim = <v_curr, v_i> / (||v_curr|| ||v_i||), reading R12
         const double cs = __ddiv_rn(__ll2double_rn(dot), __dsqrt_rn(__dmul_rn(n2k, __ll2double_rn(a.ws.n2[gj]))));
         if (cs > a.tau_s) {                                // strict: "exceeding"
@@ -502,7 +536,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       if (base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
       sm.jasc[r] = sm.js[r];
     }
-    if (threadIdx.x == 0) { sm.acc_t = 0; sm.acc_p = 0; }
+    if (threadIdx.x == 0) { sm.acc_t = 0u; sm.acc_p = 0u; }
     __syncthreads();
     // a4: count targets and deduplicated pairs of this step
     DBG_T(4);
@@ -519,7 +553,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       my_t += kept > 0 ? 1 : 0;
       my_p += kept;
     }
-    if (lane == 0) { atomicAdd((unsigned long long*)&sm.acc_t, (unsigned long long)my_t); atomicAdd((unsigned long long*)&sm.acc_p, (unsigned long long)my_p); }
+    if (lane == 0) { atomicAdd(&sm.acc_t, (uint32_t)my_t); atomicAdd(&sm.acc_p, (uint32_t)my_p); }
     __syncthreads();
     DBG_T(6);
     if (threadIdx.x == 0) {
@@ -630,6 +664,11 @@ __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
 
 using namespace ms;
 
+extern "C" int memshare_debug_stage1_tok(long long* host, int n) {
+  if (n > 2048 * 32) n = 2048 * 32;
+  return (int)cudaMemcpyFromSymbol(host, g_dbg_tok, (size_t)n * sizeof(long long));
+}
+
 // Tuning only, not part of the public ABI: copy the stage1 phase timestamps to the host.
 extern "C" int memshare_debug_stage1_times(unsigned long long* host, int n) {
   if (n > 2048 * kDbgSlots) n = 2048 * kDbgSlots;
@@ -695,6 +734,7 @@ extern "C" memshare_status memshare_step_candidates(
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem));
+    cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemSlots * sizeof(int2)));
     cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FillSmem));
     attr_set = true;
   }
@@ -706,7 +746,7 @@ extern "C" memshare_status memshare_step_candidates(
   const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
   const int grid_s1 = (int)(gcap < sms ? gcap : sms);      // 1024-thread CTAs: one per SM, one wave
-  encode_kernel<<<grid_enc, kNT, 0, st>>>(a);
+  encode_kernel<<<grid_enc, kNT, kSmemSlots * sizeof(int2), st>>>(a);
   stage1_kernel<<<grid_s1, kNT1, sizeof(SelSmem), st>>>(a);
   fill_kernel<<<grid_sel, kNT, sizeof(FillSmem), st>>>(a);
   return launch_status();

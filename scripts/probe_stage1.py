@@ -21,7 +21,7 @@ path = MemSharePath(b.tokens, b.seq_tok_off, b.gen_start, b.final, b.delim_ids, 
                     w.free_count, None, None, 0, 0, w.num_blocks, sh.num_layers, sh.num_kv_heads, sh.num_kv_heads,
                     sh.head_dim, sh.block_size)
 path.autosize(w.tau_s)
-for _ in range(5):
+for _ in range(300):
     path.segment()
     path.candidates(w.tau_s)
 torch.cuda.synchronize()
@@ -44,3 +44,32 @@ for i, n in enumerate(names[:8]):
     d = (rel[:, i + 1] - rel[:, i]) / 1e3 if i < 7 else None
     if d is not None:
         print(f"  {n:14s} -> {names[i + 1]:14s}: median {np.median(d):6.2f} us  max {d.max():6.2f} us")
+
+d1 = (act[:, 10] - act[:, 1]) / 1e3
+d2 = (act[:, 11] - act[:, 10]) / 1e3
+d3 = (act[:, 2] - act[:, 11]) / 1e3
+print("table->stage hist: median %.2f max %.2f; stream: median %.2f max %.2f; select: median %.2f max %.2f" %
+      (np.median(d1), d1.max(), np.median(d2), d2.max(), np.median(d3), d3.max()))
+
+print("raw stamps 10..14 of 4 CTAs:\n", (act[:4, 10:15] - t0))
+a12 = act[:, 12]; a13 = act[:, 13]; a14 = act[:, 14]
+ok = (a12 > 0) & (a14 > a12)
+if not ok.any():
+    ok = None
+if ok is not None: print("thread0 first run: loads %.2f us, process %.2f us (median over CTAs); max loads %.2f, max process %.2f" %
+      (np.median((a13 - a12)[ok]) / 1e3, np.median((a14 - a13)[ok]) / 1e3, ((a13 - a12)[ok]).max() / 1e3, ((a14 - a13)[ok]).max() / 1e3))
+if ok is not None: print("stream start offset from kernel start (median, max):", np.median((a12 - t0)[ok]) / 1e3, ((a12 - t0)[ok]).max() / 1e3)
+
+if ok is not None:
+  cyc = act[:, 15][ok]; ns = (a14 - a13)[ok]
+  print("effective SM clock during processing: median %.0f MHz" % np.median(cyc / np.maximum(ns, 1) * 1e3))
+
+tk = np.zeros(2048 * 32, np.int64)
+L.lib.memshare_debug_stage1_tok.argtypes = [ctypes.c_void_p, ctypes.c_int]
+L.lib.memshare_debug_stage1_tok(tk.ctypes.data, tk.size)
+tk = tk.reshape(2048, 32)
+for c in (1, 60, 122, 135):
+    row = tk[c]
+    st = row[31]
+    d = np.diff(np.concatenate([[st], row[:30][row[:30] > 0]]))
+    print("CTA", c, "per-token cycles:", d[:16].tolist())
