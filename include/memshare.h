@@ -230,6 +230,32 @@ memshare_status memshare_remap(int32_t* block_table, int32_t table_stride, int32
                                size_t workspace_bytes, int32_t* device_status, void* stream);
 size_t memshare_remap_workspace_size(int32_t num_blocks, int64_t target_cap);
 
+/* ---------------------------------------------------------------------------------------- f4
+ * Similarity ratio (Fig. 2: "the proportion of reasoning steps whose cosine
+ * similarity with any previous step exceeds a specified threshold"). From memshare_step_candidates'
+ * matches (run with that threshold as tau_s, cur_mode ALL, any top_k >= 1): redundant_steps[s] =
+ * number of steps of sequence s with a rank-0 match; ratio_s = redundant_steps[s] /
+ * (seq_step_off[s+1] - seq_step_off[s]) (step 0 never counts: it has no history).
+ *   matches [match_cap], num_matches int64 (device); redundant_steps int64 [num_seqs] (device, out) */
+memshare_status memshare_similarity_ratio(const memshare_step_match* matches, const int64_t* num_matches,
+                                          int64_t match_cap, int32_t num_seqs, int64_t* redundant_steps,
+                                          int32_t* device_status, void* stream);
+
+/* ---------------------------------------------------------------------------------------- f3
+ * All block pairs of per-sequence logical-block windows (Observation 2: "block-wise
+ * Euclidean distance between KV caches" heatmaps; SPEC.md:271-279 all-pairs oracle): for each
+ * sequence s, every pair (i, j) with blk_begin[s] <= i < j < min(blk_end[s], full blocks of s),
+ * target j / source i, grouped by target (ascending (s, j)), sources ascending; physical ids from
+ * block_table. Score with memshare_block_distance (pair_cap >= sum m(m-1)/2); D(i,j) = D(j,i).
+ *   seq_tok_off int64 [num_seqs+1]; blk_begin/blk_end int32 [num_seqs] (device); outputs as for
+ *   memshare_step_candidates (pairs, num_pairs, target_off, num_targets; CAPACITY semantics). */
+memshare_status memshare_all_pairs(const int64_t* seq_tok_off, int32_t num_seqs, const int32_t* blk_begin,
+                                   const int32_t* blk_end, const int32_t* block_table, int32_t table_stride,
+                                   int32_t num_blocks, int32_t block_size, memshare_block_pair* pairs, int64_t pair_cap,
+                                   int64_t* num_pairs, int64_t* target_off, int64_t target_cap, int64_t* num_targets,
+                                   void* workspace, size_t workspace_bytes, int32_t* device_status, void* stream);
+size_t memshare_all_pairs_workspace_size(int32_t num_seqs);
+
 /* Human-readable name of a status code (static string). */
 const char* memshare_status_string(memshare_status status);
 /* MEMSHARE_ABI_VERSION of the loaded library. */

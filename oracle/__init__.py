@@ -61,6 +61,10 @@ def lib():
         L.oracle_select.restype = None
         L.oracle_remap.argtypes = [P, I32, P, I32, P, P, P, P, P, P, I64, I32, P, P]
         L.oracle_remap.restype = ctypes.c_int
+        L.oracle_similarity_ratio.argtypes = [P, P, I64, I32, P]
+        L.oracle_similarity_ratio.restype = None
+        L.oracle_all_pairs.argtypes = [P, I32, P, P, P, I32, I32] + [P] * 6 + [I64, P, I64, P]
+        L.oracle_all_pairs.restype = I64
         _lib = L
     return _lib
 
@@ -199,3 +203,30 @@ def remap(table, refcount, free_list, free_count, dec, block_size):
     st = lib().oracle_remap(_p(tab), tab.shape[1], _p(rc), rc.size, _p(fl), _p(fc), _p(ds), _p(dt), _p(dp), _p(da),
                             ds.size, block_size, _p(nf), _p(af))
     return st, tab, rc, fl, int(fc[0]), int(nf[0]), int(af[0])
+
+
+# ---------------------------------------------------------------- f4 similarity ratio
+def similarity_ratio_counts(matches, num_seqs):
+    """Per-sequence number of steps with a Stage-1 survivor (numerator of PAPER.md:121-126)."""
+    ms, mr = _c(matches["seq"], np.int32), _c(matches["rank"], np.int32)
+    out = np.zeros(max(num_seqs, 1), np.int64)
+    lib().oracle_similarity_ratio(_p(ms), _p(mr), ms.size, num_seqs, _p(out))
+    return out[:num_seqs]
+
+
+# ---------------------------------------------------------------- f3 all pairs
+def all_pairs(seq_tok_off, blk_begin, blk_end, table, block_size):
+    off, bb, be, tab = _c(seq_tok_off, np.int64), _c(blk_begin, np.int32), _c(blk_end, np.int32), _c(table, np.int32)
+    S = bb.size
+    cap = 16
+    while True:
+        p = [np.zeros(cap, np.int32) for _ in range(6)]
+        toff = np.zeros(cap + 1, np.int64)
+        nt = np.zeros(1, np.int64)
+        n = lib().oracle_all_pairs(_p(off), S, _p(bb), _p(be), _p(tab), tab.shape[1], block_size, *[_p(a) for a in p],
+                                   cap, _p(toff), cap, _p(nt))
+        if n <= cap and nt[0] <= cap:
+            break
+        cap = max(n, int(nt[0])) + 1
+    names_p = ["seq", "target_idx", "target_logical", "source_logical", "target_phys", "source_phys"]
+    return {"pairs": {k: a[:n].copy() for k, a in zip(names_p, p)}, "target_off": toff[:int(nt[0]) + 1].copy()}

@@ -417,3 +417,51 @@ done:
   free(old_of);
   return rc;
 }
+
+/* ------------------------------------------------------------------------------------
+ * f4. Similarity ratio numerator ("the proportion of reasoning steps whose
+ * cosine similarity with any previous step exceeds a specified threshold"): per sequence, the
+ * number of current steps k with max_{j<k} cos(k, j) > tau, i.e. with at least one Stage-1
+ * survivor in the match list produced at that tau (rank 0 present).
+ * ------------------------------------------------------------------------------------ */
+void oracle_similarity_ratio(const int32_t* m_seq, const int32_t* m_rank, int64_t M, int32_t num_seqs,
+                             int64_t* redundant_steps) {
+  for (int32_t s = 0; s < num_seqs; ++s) redundant_steps[s] = 0;
+  for (int64_t i = 0; i < M; ++i)
+    if (m_rank[i] == 0) redundant_steps[m_seq[i]] += 1;
+}
+
+/* ------------------------------------------------------------------------------------
+ * f3. All block pairs of per-sequence windows (Observation 2 heatmaps;
+ * SPEC.md:271-279): for each sequence, every (i, j), i < j, of the logical blocks in
+ * [blk_begin, min(blk_end, full blocks)), target j, source i, target-major, sources ascending.
+ * Returns the pair count (written only below pair_cap); target_off gets T+1 entries.
+ * ------------------------------------------------------------------------------------ */
+int64_t oracle_all_pairs(const int64_t* seq_tok_off, int32_t num_seqs, const int32_t* blk_begin,
+                         const int32_t* blk_end, const int32_t* block_table, int32_t table_stride,
+                         int32_t block_size, int32_t* p_seq, int32_t* p_tidx, int32_t* p_tl, int32_t* p_sl,
+                         int32_t* p_tp, int32_t* p_sp, int64_t pair_cap, int64_t* target_off, int64_t target_cap,
+                         int64_t* num_targets) {
+  int64_t P = 0, T = 0;
+  for (int32_t s = 0; s < num_seqs; ++s) {
+    const int32_t full = (int32_t)((seq_tok_off[s + 1] - seq_tok_off[s]) / block_size);
+    const int32_t lo = blk_begin[s] < 0 ? 0 : blk_begin[s];
+    int32_t hi = blk_end[s] > full ? full : blk_end[s];
+    if (hi < lo) hi = lo;
+    for (int32_t j = lo + 1; j < hi; ++j) {
+      if (T < target_cap) target_off[T] = P;
+      for (int32_t i = lo; i < j; ++i) {
+        if (P < pair_cap) {
+          p_seq[P] = s; p_tidx[P] = (int32_t)T; p_tl[P] = j; p_sl[P] = i;
+          p_tp[P] = block_table[(int64_t)s * table_stride + j];
+          p_sp[P] = block_table[(int64_t)s * table_stride + i];
+        }
+        P++;
+      }
+      T++;
+    }
+  }
+  if (T <= target_cap) target_off[T] = P;
+  *num_targets = T;
+  return P;
+}

@@ -67,6 +67,12 @@ def _load():
     L.memshare_remap.restype = I32
     L.memshare_remap_workspace_size.argtypes = [I32, I64]
     L.memshare_remap_workspace_size.restype = U64
+    L.memshare_similarity_ratio.argtypes = [P, P, I64, I32, P, P, P]
+    L.memshare_similarity_ratio.restype = I32
+    L.memshare_all_pairs.argtypes = [P, I32, P, P, P, I32, I32, I32, P, I64, P, P, I64, P, P, U64, P, P]
+    L.memshare_all_pairs.restype = I32
+    L.memshare_all_pairs_workspace_size.argtypes = [I32]
+    L.memshare_all_pairs_workspace_size.restype = U64
     L.memshare_status_string.argtypes = [I32]
     L.memshare_status_string.restype = ctypes.c_char_p
     L.memshare_abi_version.argtypes = []
@@ -163,3 +169,23 @@ def remap(block_table, table_stride, num_seqs, refcount, num_blocks, free_list, 
                               _ptr(num_freed), _ptr(affected_tokens), _ptr(workspace),
                               0 if workspace is None else workspace.numel() * workspace.element_size(),
                               _ptr(device_status), _stream(stream))
+
+
+# -------------------------------------------------------------------------------------- f4
+def similarity_ratio(matches, num_matches, match_cap, num_seqs, redundant_steps, device_status, stream=None) -> int:
+    return lib.memshare_similarity_ratio(_ptr(matches), _ptr(num_matches), match_cap, num_seqs, _ptr(redundant_steps),
+                                         _ptr(device_status), _stream(stream))
+
+
+# -------------------------------------------------------------------------------------- f3
+def all_pairs_workspace_size(num_seqs: int) -> int:
+    return lib.memshare_all_pairs_workspace_size(num_seqs)
+
+
+def all_pairs(seq_tok_off, num_seqs, blk_begin, blk_end, block_table, table_stride, num_blocks, block_size, pairs,
+              pair_cap, num_pairs, target_off, target_cap, num_targets, workspace, device_status, stream=None) -> int:
+    return lib.memshare_all_pairs(_ptr(seq_tok_off), num_seqs, _ptr(blk_begin), _ptr(blk_end), _ptr(block_table),
+                                  table_stride, num_blocks, block_size, _ptr(pairs), pair_cap, _ptr(num_pairs),
+                                  _ptr(target_off), target_cap, _ptr(num_targets), _ptr(workspace),
+                                  0 if workspace is None else workspace.numel() * workspace.element_size(),
+                                  _ptr(device_status), _stream(stream))

@@ -29,7 +29,6 @@ namespace {
 constexpr int kNT = 256;          // encode / fill
 constexpr int kNT1 = 1024;        // stage1 (one CTA per current step: widest history stream)
 constexpr int kNW1 = kNT1 / 32;
-constexpr int kTokRun = 16;      // tokens per thread-run in the stage-1 history stream
 constexpr int kNW = kNT / 32;
 constexpr int kSmemSlots = 8192;       // smem hash table (steps with <= 2048 content tokens, load <= 0.25)
 constexpr int kCandCap = 1024;         // survivors held per current step
@@ -165,31 +164,6 @@ __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, i
   }
   __syncthreads();
   return tb;
-}
-
-// smem-only probe (the table pointer is derived from the kernel's shared array -> LDS.64)
-__device__ __forceinline__ int32_t table_get_smem(const int2* tab, uint32_t mask, uint32_t shift, int32_t tok) {
-  uint32_t slot = hash_slot(tok, shift);
-#pragma unroll 1
-  for (uint32_t probe = 0; probe <= mask; ++probe) {
-    const int2 e = tab[slot];
-    if (e.x == tok) return e.y;
-    if (e.x == kEmpty) return 0;
-    slot = (slot + 1) & mask;
-  }
-  return 0;
-}
-
-__device__ __forceinline__ int32_t table_get(const Table& tb, int32_t tok) {
-  uint32_t slot = hash_slot(tok, tb.shift);
-#pragma unroll 1
-  for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
-    const int2 e = tb.global ? __ldcg(tb.slots + slot) : tb.slots[slot];
-    if (e.x == tok) return e.y;
-    if (e.x == kEmpty) return 0;
-    slot = (slot + 1) & tb.mask;
-  }
-  return 0;
 }
 
 __device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {

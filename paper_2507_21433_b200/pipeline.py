@@ -138,6 +138,26 @@ class MemSharePath:
                         self.free_count, self.decisions, self.num_targets, self.caps.target, self.block_size,
                         self.num_freed, self.affected, self.workspace, self.status, self.stream), "remap")
 
+    # ------------------------------------------------------------------ analysis (f3, f4)
+    def similarity_ratio(self):
+        """f4: per-sequence count of steps with a Stage-1 survivor (run candidates() first with the
+        threshold of interest); returns the device int64 [num_seqs] tensor."""
+        out = torch.zeros(max(1, self.num_seqs), dtype=torch.int64, device=self.dev)
+        L.check(L.similarity_ratio(self.matches, self.num_matches, self.caps.match, self.num_seqs, out, self.status,
+                                   self.stream), "similarity_ratio")
+        return out[:self.num_seqs]
+
+    def all_pairs(self, blk_begin, blk_end):
+        """f3: fill the pair buffers with every block pair of the per-sequence windows (then
+        distance_call() scores the distance matrix). Caps must hold sum m(m-1)/2 pairs."""
+        bb, be = _dev_i32(blk_begin, self.dev), _dev_i32(blk_end, self.dev)
+        self._ap_keep = (bb, be)
+        ws = torch.empty(max(1, L.all_pairs_workspace_size(self.num_seqs)), dtype=torch.uint8, device=self.dev)
+        self._ap_ws = ws
+        L.check(L.all_pairs(self.seq_tok_off, self.num_seqs, bb, be, self.table, self.table_stride, self.num_blocks,
+                            self.block_size, self.pairs, self.caps.pair, self.num_pairs, self.target_off,
+                            self.caps.target, self.num_targets, ws, self.status, self.stream), "all_pairs")
+
     def round(self, tau_s, tau_b, top_k=0, pairing=L.PAIR_ALIGNED, cur_mode=L.CUR_ALL, cur_begin=None, cur_end=None):
         self.segment()
         self.candidates(tau_s, top_k, pairing, cur_mode, cur_begin, cur_end)
