@@ -417,24 +417,39 @@ using AnchorT = float2[kR * 4];
 using AnchorT = uint4[kR];
 #endif
 
+// d = t - s in ONE mixed-precision FMA straight from the packed bf16 source (SASS FHFMA.BF16 with
+// .H0/.H1 half selection, sm_100): fma(s, -1, t) = RN(t - s) exactly as before, no unpack.
+__device__ __forceinline__ float2 sub_bf2(uint32_t x, float2 t) {
+  float2 d;
+  asm("{\n.reg .b16 lo, hi;\nmov.b32 {lo, hi}, %2;\n"
+      "fma.rn.f32.bf16 %0, lo, %5, %3;\nfma.rn.f32.bf16 %1, hi, %5, %4;\n}\n"
+      : "=f"(d.x), "=f"(d.y)
+      : "r"(x), "f"(t.x), "f"(t.y), "h"((unsigned short)0xBF80u));
+  return d;
+}
+
 template <int K>
 __device__ __forceinline__ float dist2_anchor(const AnchorT (&A)[kAnchors], const uint4 (&x)[kR]) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#if !MS_ANCHOR_FP32
   const float2 neg1 = make_float2(-1.f, -1.f);
+#endif
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
 #if MS_ANCHOR_FP32
-    const float2 t0 = A[K][4 * r + 0], t1 = A[K][4 * r + 1], t2 = A[K][4 * r + 2], t3 = A[K][4 * r + 3];
+    const float2 d0 = sub_bf2(x[r].x, A[K][4 * r + 0]);
+    const float2 d1 = sub_bf2(x[r].y, A[K][4 * r + 1]);
+    const float2 d2 = sub_bf2(x[r].z, A[K][4 * r + 2]);
+    const float2 d3 = sub_bf2(x[r].w, A[K][4 * r + 3]);
 #else
     const float2 t0 = bf2_to_f2(A[K][r].x), t1 = bf2_to_f2(A[K][r].y), t2 = bf2_to_f2(A[K][r].z),
                  t3 = bf2_to_f2(A[K][r].w);
-#endif
-    // d = t - s exactly rounded (fma with -1; the anchor is the register operand), acc += d*d
     const float2 d0 = __ffma2_rn(bf2_to_f2(x[r].x), neg1, t0);
     const float2 d1 = __ffma2_rn(bf2_to_f2(x[r].y), neg1, t1);
     const float2 d2 = __ffma2_rn(bf2_to_f2(x[r].z), neg1, t2);
     const float2 d3 = __ffma2_rn(bf2_to_f2(x[r].w), neg1, t3);
-    acc0 = __ffma2_rn(d0, d0, acc0);
+#endif
+    acc0 = __ffma2_rn(d0, d0, acc0);                     // acc += d*d, packed (FFMA2)
     acc1 = __ffma2_rn(d1, d1, acc1);
     acc0 = __ffma2_rn(d2, d2, acc0);
     acc1 = __ffma2_rn(d3, d3, acc1);
@@ -464,6 +479,92 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
     const int64_t total = I * a.n_chunks;
     int stage = 0;
     uint32_t ph = 0;
+    if (kAnchors == 1) {
+      // One target per item. The next unit's metadata (target range, target and source ids) is
+      // loaded into registers one unit ahead, so issuing never waits on metadata latency.
+      struct UnitMeta { int64_t lc, t; int32_t lo, np, tphys, sp0, sp1; };
+      auto load_meta = [&](int64_t u) {
+        UnitMeta m{0, 0, 0, 0, 0, 0, 0};
+        if (u >= total) return m;
+        m.lc = u / I;
+        m.t = u - m.lc * I;
+        const int64_t lo = __ldcg(a.target_off + m.t);
+        int64_t hi = __ldcg(a.target_off + m.t + 1);
+        if (hi > Pn) hi = Pn;
+        m.lo = (int32_t)lo;
+        m.np = (int32_t)(hi > lo ? hi - lo : 0);
+        if (m.np > 0) m.tphys = a.pairs[lo].target_phys;
+        if (lane < m.np) m.sp0 = a.pairs[lo + lane].source_phys;
+        if (lane + 32 < m.np) m.sp1 = a.pairs[lo + 32 + lane].source_phys;
+        return m;
+      };
+      int64_t unit = 0, next = 0;
+      if (lane == 0) {
+        unit = (int64_t)atomicAdd(a.ws.ticket, 1u);
+        next = (int64_t)atomicAdd(a.ws.ticket, 1u);
+      }
+      unit = __shfl_sync(0xffffffffu, unit, 0);
+      next = __shfl_sync(0xffffffffu, next, 0);
+      UnitMeta cur = load_meta(unit);
+      while (unit < total) {
+        int64_t next2 = 0;
+        if (lane == 0) next2 = (int64_t)atomicAdd(a.ws.ticket, 1u);
+        const UnitMeta nm = load_meta(next);                  // consumed next iteration
+        if (cur.np > 0) {
+          const int32_t tphys = checked_phys(a, cur.tphys);
+          const int32_t l0 = (int32_t)cur.lc * a.lpi;
+          const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
+          for (int32_t c0 = 0; c0 < cur.np; c0 += 64) {       // pairs in chunks of 64 (register-staged)
+            const int32_t cn = (cur.np - c0) < 64 ? cur.np - c0 : 64;
+            int32_t sa = cur.sp0, sb = cur.sp1;
+            if (c0 > 0) {
+              sa = (lane < cn) ? a.pairs[cur.lo + c0 + lane].source_phys : 0;
+              sb = (lane + 32 < cn) ? a.pairs[cur.lo + c0 + 32 + lane].source_phys : 0;
+            }
+            for (int32_t l = l0; l < l1; ++l) {
+              for (int32_t kv = 0; kv < 2; ++kv) {
+                const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
+                for (int32_t sub = 0; sub < a.n_sub; ++sub) {
+                  const int32_t boff = sub * a.sub_bytes;
+                  const int32_t bytes = (a.slice_bytes - boff) < a.sub_bytes ? (a.slice_bytes - boff) : a.sub_bytes;
+                  for (int32_t q = -1; q < cn; ++q) {          // q = -1: the target (anchor 0)
+                    const int32_t v = __shfl_sync(0xffffffffu, (q & 32) ? sb : sa, q < 0 ? 0 : (q & 31));
+                    if (lane == 0) {
+                      const int32_t phys = q < 0 ? tphys : checked_phys(a, v);
+                      mbar_wait(&sm.empty[stage], ph ^ 1u);
+                      Meta& m = sm.meta[stage];
+                      m.anchor = q < 0 ? 0 : -1;
+                      m.nent = q < 0 ? 0 : 1;
+                      m.pair[0] = cur.lo + c0 + q;
+                      m.anc[0] = 0;
+                      m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes; m.flags = 0;
+                      mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
+                      bulk_g2s(sm.ring[stage], base + (int64_t)phys * a.block_stride_b + boff, (uint32_t)bytes,
+                               &sm.full[stage]);
+                      if (++stage == kStages) { stage = 0; ph ^= 1u; }
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+        unit = next;
+        next = __shfl_sync(0xffffffffu, next2, 0);
+        cur = nm;
+      }
+      stage = __shfl_sync(0xffffffffu, stage, 0);
+      ph = __shfl_sync(0xffffffffu, ph, 0);
+      if (lane == 0) {
+        mbar_wait(&sm.empty[stage], ph ^ 1u);
+        sm.meta[stage].flags = F_STOP;
+        sm.meta[stage].nent = 0;
+        sm.meta[stage].anchor = -1;
+        mbar_arrive(&sm.full[stage]);
+      }
+      return;
+    }
     ProdSmem& ps = sm.prod;
     int64_t unit = 0;
     if (lane == 0) unit = (int64_t)atomicAdd(a.ws.ticket, 1u);
