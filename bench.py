@@ -387,6 +387,53 @@ def main():
     ms_step = ms_total / args.steps
     value = pairs_all / (ms_step / 1e3)
 
+    # ---------------------------------------------------------------- online round latency
+    # PAPER.md:317 evaluates each step as it finishes: CUR_LAST = the newly finished step of every
+    # sequence against its history (one graph replay per round; table restored each round).
+    online = None
+    if args.mode == "seq":
+        # the busiest step of each sequence (most Stage-1 survivors in the offline pass) as RANGE
+        mt = path.read_candidates()["matches"]
+        busiest = np.zeros(w.batch.num_seqs, np.int32)
+        for sq in range(w.batch.num_seqs):
+            st = mt["step"][mt["seq"] == sq]
+            if st.size:
+                busiest[sq] = np.bincount(st).argmax()
+
+        def time_round(cur_mode, cb=None, ce=None):
+            def online_round():
+                restore()
+                path.segment()
+                path.candidates(w.tau_s, cur_mode=cur_mode, cur_begin=cb, cur_end=ce)
+                path.distance_call(w.tau_b)
+                path.remap()
+            online_round()
+            torch.cuda.synchronize()
+            og = path.capture(online_round)
+            for _ in range(10):
+                og.replay()
+            torch.cuda.synchronize()
+            o_pairs = int(path.num_pairs.item())
+            o0, o1 = ev(), ev()
+            n_on = max(50, min(args.steps, 500))
+            o0.record(stream)
+            for _ in range(n_on):
+                og.replay()
+            o1.record(stream)
+            torch.cuda.synchronize()
+            return 1e3 * o0.elapsed_time(o1) / n_on, o_pairs, n_on
+
+        last_us, last_pairs, n_on = time_round(L.CUR_LAST)
+        busy_us, busy_pairs, _ = time_round(L.CUR_RANGE, busiest, busiest + 1)
+        online = {"round_us": last_us, "pairs_per_round": last_pairs,
+                  "busiest_round_us": busy_us, "busiest_pairs_per_round": busy_pairs,
+                  "current_steps_per_round": w.batch.num_seqs, "rounds": n_on,
+                  "note": "online (PAPER.md:317): one graph replay of a1-a7 with one current step per sequence -- "
+                          "round_us: the last finished step (cur_mode LAST); busiest_round_us: the step with the "
+                          "most Stage-1 survivors (cur_mode RANGE)"}
+        restore()
+        torch.cuda.synchronize()
+
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
     if not args.no_e2e:
@@ -481,7 +528,7 @@ def main():
         "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
         "clocks": {"sm_mhz": ck["sm_mhz"], "sm_max_mhz": ck["sm_max_mhz"], "reasons": ck["reasons"],
                    "samples": ck["samples"]},
-        "e2e": e2e, "cpu_baseline": cpu,
+        "e2e": e2e, "cpu_baseline": cpu, "online": online,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -74,6 +74,13 @@ typedef int32_t memshare_status;
 #define MEMSHARE_DIST_PARTIAL 1
 #define MEMSHARE_DIST_FINALIZE 2
 
+/* Stage-2 block metric. EUCLIDEAN is Alg. 1 Stage 2. COSINE is the variant the
+ * paper compares against (Fig. 7, reading R34): per layer the cosine of the K
+ * slices and of the V slices, D = 1 - (1/N) sum_l (cos_K + cos_V)/2 in [0, 2], so the same strict
+ * D < tau_b test and argmin selection apply; FULL mode only. */
+#define MEMSHARE_METRIC_EUCLIDEAN 0
+#define MEMSHARE_METRIC_COSINE 1
+
 #define MEMSHARE_MAX_DELIMS 16
 
 /* KV geometry. num_kv_heads_global is the h of Alg. 1's 2dh normaliser (reading R17); the pool
@@ -190,7 +197,7 @@ size_t memshare_step_candidates_workspace_size(int64_t num_tokens, int32_t num_s
  *   pool, dims (host structs)     geometry; pool unused in FINALIZE mode
  *   pairs, target_off, num_pairs, num_targets   memshare_step_candidates outputs (device);
  *                                 counts are clamped to pair_cap / target_cap
- *   mode FULL | PARTIAL | FINALIZE
+ *   mode FULL | PARTIAL | FINALIZE; metric EUCLIDEAN | COSINE (COSINE: FULL mode only)
  *   partial_sq float [pair_cap][N][2]   PARTIAL: output (sum over local heads of squared
  *                                 differences, [.][l][0] = K, [.][l][1] = V); FINALIZE: input;
  *                                 FULL: optional output (may be NULL)
@@ -201,12 +208,12 @@ size_t memshare_step_candidates_workspace_size(int64_t num_tokens, int32_t num_s
 memshare_status memshare_block_distance(const memshare_kv_pool* pool_host, const memshare_dims* dims_host,
                                         const memshare_block_pair* pairs, const int64_t* target_off,
                                         const int64_t* num_pairs, const int64_t* num_targets, int64_t pair_cap,
-                                        int64_t target_cap, int32_t mode, float* partial_sq, float tau_b,
+                                        int64_t target_cap, int32_t mode, int32_t metric, float* partial_sq, float tau_b,
                                         float* distance, uint8_t* under, memshare_decision* decisions,
                                         void* workspace, size_t workspace_bytes, int32_t* device_status,
                                         void* stream);
 size_t memshare_block_distance_workspace_size(const memshare_dims* dims_host, int32_t num_blocks, int64_t pair_cap,
-                                              int64_t target_cap);
+                                              int64_t target_cap, int32_t metric);
 
 /* ---------------------------------------------------------------------------------------- a7
  * Zero-copy remap (PAPER.md:276-278 "the mechanism simply updates the block table", :283-284;

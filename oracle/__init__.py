@@ -61,6 +61,8 @@ def lib():
         L.oracle_select.restype = None
         L.oracle_remap.argtypes = [P, I32, P, I32, P, P, P, P, P, P, I64, I32, P, P]
         L.oracle_remap.restype = ctypes.c_int
+        L.oracle_block_cosine.argtypes = [P, P, I64, I64, I32, I32, I32, I32, P, P, I64, P]
+        L.oracle_block_cosine.restype = None
         L.oracle_similarity_ratio.argtypes = [P, P, I64, I32, P]
         L.oracle_similarity_ratio.restype = None
         L.oracle_all_pairs.argtypes = [P, I32, P, P, P, I32, I32] + [P] * 6 + [I64, P, I64, P]
@@ -230,3 +232,14 @@ def all_pairs(seq_tok_off, blk_begin, blk_end, table, block_size):
         cap = max(n, int(nt[0])) + 1
     names_p = ["seq", "target_idx", "target_logical", "source_logical", "target_phys", "source_phys"]
     return {"pairs": {k: a[:n].copy() for k, a in zip(names_p, p)}, "target_off": toff[:int(nt[0]) + 1].copy()}
+
+
+# ---------------------------------------------------------------- f2 cosine block metric
+def block_cosine(k, v, layer_stride, block_stride, num_layers, h_local, head_dim, block_size, tphys, sphys):
+    """D_cos = 1 - mean over layers of (cos_K + cos_V)/2 (reading R34)."""
+    k, v = _c(k, np.uint16), _c(v, np.uint16)
+    tp, sp = _c(tphys, np.int32), _c(sphys, np.int32)
+    D = np.zeros(tp.size, np.float64)
+    lib().oracle_block_cosine(_p(k), _p(v), layer_stride, block_stride, num_layers, h_local, head_dim, block_size,
+                              _p(tp), _p(sp), tp.size, _p(D))
+    return D

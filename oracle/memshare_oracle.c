@@ -3,7 +3,8 @@
  * A plain, slow, single-threaded C99 reference of MemShare's collaborative-filtering
  * KV-block reuse path (arXiv 2507.21433), written from /root/reference/PAPER.md:
  *   Algorithm 1 Stage 1, Stage 2,
- *   and the zero-copy block-table sharing mechanism.
+ *   the zero-copy block-table sharing mechanism, and the cosine block
+ *   metric the paper compares Stage 2 against (f2).
  * Floating point is fp64 throughout (bf16 -> double is exact). No SIMD, no threads, no
  * blocking or reordering beyond what the definitions state. Where the paper is silent or
  * ambiguous the reading taken is the one listed in DESIGN.md §"Readings" (R-numbers below).
@@ -464,4 +465,40 @@ int64_t oracle_all_pairs(const int64_t* seq_tok_off, int32_t num_seqs, const int
   if (T <= target_cap) target_off[T] = P;
   *num_targets = T;
   return P;
+}
+
+/* ------------------------------------------------------------------------------------
+ * f2. Cosine block similarity, the Stage-2 variant the paper compares against (PAPER.md:271-273
+ * "While cosine similarity measures only angular alignment between vectors, Euclidean distance
+ * captures both directional and magnitude differences"; Fig. 7). Reading R34: per layer the
+ * cosine of the flattened K slices and of the V slices; D = 1 - (1/N) sum_l (cos_K + cos_V)/2,
+ * so that smaller is more similar like Alg. 1's D. Two all-zero slices have cosine 1, one
+ * all-zero slice cosine 0.
+ * ------------------------------------------------------------------------------------ */
+static double slice_cos(const uint16_t* a, const uint16_t* b, int64_t n) {
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  for (int64_t e = 0; e < n; ++e) {
+    const double x = bf16_to_double(a[e]), y = bf16_to_double(b[e]);
+    dot += x * y;
+    na += x * x;
+    nb += y * y;
+  }
+  if (na == 0.0 && nb == 0.0) return 1.0;
+  if (na == 0.0 || nb == 0.0) return 0.0;
+  return dot / sqrt(na * nb);
+}
+
+void oracle_block_cosine(const uint16_t* k, const uint16_t* v, int64_t layer_stride, int64_t block_stride,
+                         int32_t num_layers, int32_t h_local, int32_t head_dim, int32_t block_size,
+                         const int32_t* tphys, const int32_t* sphys, int64_t P, double* D) {
+  const int64_t slice = (int64_t)block_size * h_local * head_dim;
+  for (int64_t p = 0; p < P; ++p) {
+    double acc = 0.0;
+    for (int32_t l = 0; l < num_layers; ++l) {
+      const int64_t ot = (int64_t)l * layer_stride + (int64_t)tphys[p] * block_stride;
+      const int64_t os = (int64_t)l * layer_stride + (int64_t)sphys[p] * block_stride;
+      acc += 0.5 * (slice_cos(k + ot, k + os, slice) + slice_cos(v + ot, v + os, slice));
+    }
+    D[p] = 1.0 - acc / num_layers;
+  }
 }

@@ -20,6 +20,7 @@ OK, INVALID_ARGUMENT, CAPACITY, CORRUPTION, CUDA_ERROR = 0, 1, 2, 3, 4
 CUR_ALL, CUR_LAST, CUR_RANGE = 0, 1, 2
 PAIR_ALIGNED, PAIR_CROSS = 0, 1
 DIST_FULL, DIST_PARTIAL, DIST_FINALIZE = 0, 1, 2
+METRIC_EUCLIDEAN, METRIC_COSINE = 0, 1
 
 MATCH_DTYPE = np.dtype([("seq", "<i4"), ("step", "<i4"), ("cand_step", "<i4"), ("rank", "<i4"), ("cosine", "<f8")])
 PAIR_DTYPE = np.dtype([("seq", "<i4"), ("target_idx", "<i4"), ("target_logical", "<i4"), ("source_logical", "<i4"),
@@ -59,9 +60,9 @@ def _load():
     L.memshare_step_candidates.restype = I32
     L.memshare_step_candidates_workspace_size.argtypes = [I64, I32, I64, I64]
     L.memshare_step_candidates_workspace_size.restype = U64
-    L.memshare_block_distance.argtypes = [P, P, P, P, P, P, I64, I64, I32, P, F32, P, P, P, P, U64, P, P]
+    L.memshare_block_distance.argtypes = [P, P, P, P, P, P, I64, I64, I32, I32, P, F32, P, P, P, P, U64, P, P]
     L.memshare_block_distance.restype = I32
-    L.memshare_block_distance_workspace_size.argtypes = [P, I32, I64, I64]
+    L.memshare_block_distance_workspace_size.argtypes = [P, I32, I64, I64, I32]
     L.memshare_block_distance_workspace_size.restype = U64
     L.memshare_remap.argtypes = [P, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, P, U64, P, P]
     L.memshare_remap.restype = I32
@@ -143,15 +144,17 @@ def step_candidates(tokens, num_tokens, seq_tok_off, num_seqs, seq_step_off, ste
 
 
 # ----------------------------------------------------------------------------------- a5-a6
-def block_distance_workspace_size(dims: Dims, num_blocks: int, pair_cap: int, target_cap: int) -> int:
-    return lib.memshare_block_distance_workspace_size(ctypes.byref(dims), num_blocks, pair_cap, target_cap)
+def block_distance_workspace_size(dims: Dims, num_blocks: int, pair_cap: int, target_cap: int,
+                                  metric: int = METRIC_EUCLIDEAN) -> int:
+    return lib.memshare_block_distance_workspace_size(ctypes.byref(dims), num_blocks, pair_cap, target_cap, metric)
 
 
 def block_distance(pool: KVPool | None, dims: Dims, pairs, target_off, num_pairs, num_targets, pair_cap, target_cap,
-                   mode, partial_sq, tau_b, distance, under, decisions, workspace, device_status, stream=None) -> int:
+                   mode, partial_sq, tau_b, distance, under, decisions, workspace, device_status, stream=None,
+                   metric: int = METRIC_EUCLIDEAN) -> int:
     return lib.memshare_block_distance(
         None if pool is None else ctypes.byref(pool), ctypes.byref(dims), _ptr(pairs), _ptr(target_off),
-        _ptr(num_pairs), _ptr(num_targets), pair_cap, target_cap, mode, _ptr(partial_sq), float(tau_b),
+        _ptr(num_pairs), _ptr(num_targets), pair_cap, target_cap, mode, metric, _ptr(partial_sq), float(tau_b),
         _ptr(distance), _ptr(under), _ptr(decisions), _ptr(workspace),
         0 if workspace is None else workspace.numel() * workspace.element_size(), _ptr(device_status),
         _stream(stream))

@@ -90,12 +90,15 @@ struct DistWs {
   ItemRec* items;        // [item_cap]
   int32_t* cnt;          // [target_cap] items starting at each sorted position
   int64_t* item_off;     // [target_cap + 1]
-  float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]
+  float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]  squared sums (Euclidean) / dot (cosine)
+  float* wsn;            // cosine only: [pair_cap][N][2][n_sub][W] source squared norms
+  float* wtn;            // cosine only: [target_cap][N][2][n_sub][W] target squared norms
 };
 
 int64_t item_cap_of(int64_t pair_cap, int64_t target_cap) { return target_cap + pair_cap / kItemPairs + 2; }
 
-DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t num_blocks, int64_t pair_cap, int64_t target_cap) {
+DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t num_blocks, int64_t pair_cap, int64_t target_cap,
+                   int32_t metric) {
   (void)num_blocks;
   DistWs d;
   d.ticket = w.take<unsigned int>(1);
@@ -103,7 +106,11 @@ DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t num_blocks, int64_t 
   d.items = w.take<ItemRec>(item_cap_of(pair_cap, target_cap));
   d.cnt = w.take<int32_t>(target_cap + 1);
   d.item_off = w.take<int64_t>(target_cap + 2);
-  d.wpart = w.take<float>((size_t)pair_cap * N * 2 * n_sub * kConsumerWarps + 1);
+  const size_t per = (size_t)N * 2 * n_sub * kConsumerWarps;
+  d.wpart = w.take<float>((size_t)pair_cap * per + 1);
+  const bool cosine = metric == MEMSHARE_METRIC_COSINE;
+  d.wsn = w.take<float>(cosine ? (size_t)pair_cap * per + 1 : 1);
+  d.wtn = w.take<float>(cosine ? (size_t)target_cap * per + 1 : 1);
   return d;
 }
 
@@ -123,6 +130,7 @@ struct DistArgs {
   const int64_t* num_targets;
   int64_t pair_cap, target_cap;
   int32_t mode;
+  int32_t metric;        // MEMSHARE_METRIC_EUCLIDEAN | MEMSHARE_METRIC_COSINE
   float* partial_sq;
   float tau_b;
   float* distance;
@@ -200,10 +208,9 @@ __device__ __forceinline__ int64_t clamp_count(const int64_t* p, int64_t cap) {
   return v < 0 ? 0 : (v < cap ? v : cap);
 }
 
-// fixed-order fp32 sum of the per-warp partials of (pair p, layer l, kv)
-__device__ __forceinline__ float sum_part(const DistArgs& a, int64_t p, int32_t l, int32_t kv, bool from_partial) {
-  if (from_partial) return __ldcg(a.partial_sq + ((p * a.N + l) * 2 + kv));
-  const float4* w = reinterpret_cast<const float4*>(a.ws.wpart + (((p * a.N + l) * 2 + kv) * a.n_sub) * kConsumerWarps);
+// fixed-order fp32 sum of the per-warp partials of (row, layer l, kv) of one workspace buffer
+__device__ __forceinline__ float sum_warps(const DistArgs& a, const float* buf, int64_t row, int32_t l, int32_t kv) {
+  const float4* w = reinterpret_cast<const float4*>(buf + (((row * a.N + l) * 2 + kv) * a.n_sub) * kConsumerWarps);
   float s = 0.f;
   for (int sub = 0; sub < a.n_sub; ++sub) {
     float4 v[kConsumerWarps / 4];
@@ -213,6 +220,18 @@ __device__ __forceinline__ float sum_part(const DistArgs& a, int64_t p, int32_t 
     for (int j = 0; j < kConsumerWarps / 4; ++j) s = (((s + v[j].x) + v[j].y) + v[j].z) + v[j].w;
   }
   return s;
+}
+
+__device__ __forceinline__ float sum_part(const DistArgs& a, int64_t p, int32_t l, int32_t kv, bool from_partial) {
+  if (from_partial) return __ldcg(a.partial_sq + ((p * a.N + l) * 2 + kv));
+  return sum_warps(a, a.ws.wpart, p, l, kv);
+}
+
+// cosine of one (pair, layer, K|V) from fp32 dot and squared norms, in fp64 (f2 metric, reading R34)
+__device__ __forceinline__ double cos_of(float dot, float tn, float sn) {
+  if (tn == 0.f && sn == 0.f) return 1.0;               // two zero slices are identical
+  if (tn == 0.f || sn == 0.f) return 0.0;
+  return (double)dot / __dsqrt_rn((double)tn * (double)sn);
 }
 
 // Finalise target t with the kConsumers threads (tid in [0, kConsumers)); `sync` is the barrier
@@ -231,14 +250,21 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
     const int64_t p = pc + tid / N;
     const int32_t l = tid % N;
     if (tid < ppc * N && p < p1) {
-      const float sk = sum_part(a, p, l, 0, from_partial);
-      const float sv = sum_part(a, p, l, 1, from_partial);
-      if (!from_partial && a.partial_sq != nullptr) {
-        a.partial_sq[(p * N + l) * 2 + 0] = sk;
-        a.partial_sq[(p * N + l) * 2 + 1] = sv;
+      if (a.metric == MEMSHARE_METRIC_COSINE) {
+        // f2: PAPER.md:271-273 cosine block similarity, averaged over K|V and layers
+        const double ck = cos_of(sum_part(a, p, l, 0, false), sum_warps(a, a.ws.wtn, t, l, 0), sum_warps(a, a.ws.wsn, p, l, 0));
+        const double cv = cos_of(sum_part(a, p, l, 1, false), sum_warps(a, a.ws.wtn, t, l, 1), sum_warps(a, a.ws.wsn, p, l, 1));
+        terms[tid] = 0.5 * (ck + cv);
+      } else {
+        const float sk = sum_part(a, p, l, 0, from_partial);
+        const float sv = sum_part(a, p, l, 1, from_partial);
+        if (!from_partial && a.partial_sq != nullptr) {
+          a.partial_sq[(p * N + l) * 2 + 0] = sk;
+          a.partial_sq[(p * N + l) * 2 + 1] = sv;
+        }
+        // Alg. 1 line 5: (Delta_K + Delta_V) / (2dh)
+        terms[tid] = (__dsqrt_rn((double)sk) + __dsqrt_rn((double)sv)) * inv;
       }
-      // Alg. 1 line 5: (Delta_K + Delta_V) / (2dh)
-      terms[tid] = (__dsqrt_rn((double)sk) + __dsqrt_rn((double)sv)) * inv;
     }
     sync();
     if (a.mode != MEMSHARE_DIST_PARTIAL) {
@@ -249,7 +275,8 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
         for (int l2 = lane; l2 < N; l2 += 32) acc += terms[q * N + l2];
         acc = warp_sum(acc);
         if (lane == 0) {
-          const float D = (float)(acc / (double)N);     // Alg. 1 line 7: return D / N
+          // Alg. 1 line 7: return D / N  (cosine metric: D = 1 - mean similarity)
+          const float D = (float)(a.metric == MEMSHARE_METRIC_COSINE ? 1.0 - acc / (double)N : acc / (double)N);
           a.distance[pp] = D;
           a.under[pp] = D < a.tau_b ? 1 : 0;
         }
@@ -457,6 +484,7 @@ __device__ __forceinline__ float dist2_anchor(const AnchorT (&A)[kAnchors], cons
   return (acc0.x + acc0.y) + (acc1.x + acc1.y);
 }
 
+template <int kMetric>
 __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   DistSmem& sm = *reinterpret_cast<DistSmem*>(smem_raw);
@@ -535,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
                       Meta& m = sm.meta[stage];
                       m.anchor = q < 0 ? 0 : -1;
                       m.nent = q < 0 ? 0 : 1;
-                      m.pair[0] = cur.lo + c0 + q;
+                      m.pair[0] = q < 0 ? (int32_t)cur.t : cur.lo + c0 + q;   // target slot: target index
                       m.anc[0] = 0;
                       m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes; m.flags = 0;
                       mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
@@ -721,6 +749,40 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
     if (lane == 0) mbar_arrive(&sm.empty[stage]);            // stage free: data is in registers
     if (++stage == kStages) { stage = 0; ph ^= 1u; }
     if (MS_DIAG_NO_COMPUTE) continue;
+    if (kMetric == MEMSHARE_METRIC_COSINE) {
+      // f2 (kAnchors == 1): target slot -> cache + squared norm; source slot -> dot + squared norm
+      float2 n0 = make_float2(0.f, 0.f), n1 = make_float2(0.f, 0.f);
+      if (anchor >= 0) {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
+          A[0][4 * r + 0] = f0; A[0][4 * r + 1] = f1; A[0][4 * r + 2] = f2; A[0][4 * r + 3] = f3;
+          n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
+          n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
+        }
+        float tn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
+        if (lane == 0)
+          a.ws.wtn[((((int64_t)(ent[0] >> 2) * a.N + layer) * 2 + kv) * a.n_sub + sub) * kConsumerWarps + warp] = tn;
+      } else if (nent > 0) {
+        float2 d0 = make_float2(0.f, 0.f), d1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
+          d0 = __ffma2_rn(A[0][4 * r + 0], f0, d0); d1 = __ffma2_rn(A[0][4 * r + 1], f1, d1);
+          d0 = __ffma2_rn(A[0][4 * r + 2], f2, d0); d1 = __ffma2_rn(A[0][4 * r + 3], f3, d1);
+          n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
+          n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
+        }
+        const float dot = warp_sum((d0.x + d0.y) + (d1.x + d1.y));
+        const float sn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
+        if (lane == 0) {
+          const int64_t o = ((((int64_t)(ent[0] >> 2) * a.N + layer) * 2 + kv) * a.n_sub + sub) * kConsumerWarps + warp;
+          a.ws.wpart[o] = dot;
+          a.ws.wsn[o] = sn;
+        }
+      }
+      continue;
+    }
     if (anchor >= 0) {
 #pragma unroll
       for (int j = 0; j < kAnchors; ++j)
@@ -783,11 +845,12 @@ static int32_t n_sub_of(int64_t slice_bytes) {
 }
 
 extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* dims, int32_t num_blocks,
-                                                         int64_t pair_cap, int64_t target_cap) {
+                                                         int64_t pair_cap, int64_t target_cap, int32_t metric) {
   if (!dims || pair_cap < 0 || target_cap < 0 || num_blocks < 0 || dims->num_layers < 1) return 0;
+  if (metric != MEMSHARE_METRIC_EUCLIDEAN && metric != MEMSHARE_METRIC_COSINE) return 0;
   const int64_t slice = (int64_t)dims->block_size * dims->num_kv_heads_local * dims->head_dim * 2;
   Ws w{nullptr, 0};
-  dist_layout(w, dims->num_layers, n_sub_of(slice), num_blocks, pair_cap, target_cap);
+  dist_layout(w, dims->num_layers, n_sub_of(slice), num_blocks, pair_cap, target_cap, metric);
   return w.size();
 }
 
@@ -795,12 +858,16 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
                                                    const memshare_block_pair* pairs, const int64_t* target_off,
                                                    const int64_t* num_pairs, const int64_t* num_targets,
                                                    int64_t pair_cap, int64_t target_cap, int32_t mode,
-                                                   float* partial_sq, float tau_b, float* distance, uint8_t* under,
+                                                   int32_t metric, float* partial_sq, float tau_b, float* distance,
+                                                   uint8_t* under,
                                                    memshare_decision* decisions, void* workspace,
                                                    size_t workspace_bytes, int32_t* device_status, void* stream) {
   if (!dims || !pairs || !target_off || !num_pairs || !num_targets || !workspace || !device_status)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (mode < MEMSHARE_DIST_FULL || mode > MEMSHARE_DIST_FINALIZE) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (metric != MEMSHARE_METRIC_EUCLIDEAN && metric != MEMSHARE_METRIC_COSINE) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (metric == MEMSHARE_METRIC_COSINE && (mode != MEMSHARE_DIST_FULL || kAnchors != 1))
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (pair_cap < 0 || pair_cap > ((int64_t)1 << 30) || target_cap < 0 || target_cap > (int64_t)INT32_MAX)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   const memshare_dims dm = *dims;
@@ -820,7 +887,7 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
       return MEMSHARE_ERR_INVALID_ARGUMENT;
     num_blocks = pool->num_blocks;
   }
-  if (workspace_bytes < memshare_block_distance_workspace_size(dims, num_blocks, pair_cap, target_cap))
+  if (workspace_bytes < memshare_block_distance_workspace_size(dims, num_blocks, pair_cap, target_cap, metric))
     return MEMSHARE_ERR_INVALID_ARGUMENT;
 
   DistArgs a{};
@@ -845,10 +912,10 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   if (a.lpi > a.N) a.lpi = a.N;
   a.n_chunks = (a.N + a.lpi - 1) / a.lpi;
   a.pairs = pairs; a.target_off = target_off; a.num_pairs = num_pairs; a.num_targets = num_targets;
-  a.pair_cap = pair_cap; a.target_cap = target_cap; a.mode = mode; a.partial_sq = partial_sq; a.tau_b = tau_b;
+  a.pair_cap = pair_cap; a.target_cap = target_cap; a.mode = mode; a.metric = metric; a.partial_sq = partial_sq; a.tau_b = tau_b;
   a.distance = distance; a.under = under; a.decisions = decisions; a.status = device_status;
   Ws w{static_cast<char*>(workspace), 0};
-  a.ws = dist_layout(w, a.N, a.n_sub, num_blocks, pair_cap, target_cap);
+  a.ws = dist_layout(w, a.N, a.n_sub, num_blocks, pair_cap, target_cap, metric);
   {
     int64_t np2 = 1;
     while (np2 < target_cap && np2 < kPlanSortCap) np2 <<= 1;
@@ -864,8 +931,10 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   }
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(distance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DistSmem)) !=
-            cudaSuccess ||
+    if (cudaFuncSetAttribute(distance_kernel<MEMSHARE_METRIC_EUCLIDEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(DistSmem)) != cudaSuccess ||
+        cudaFuncSetAttribute(distance_kernel<MEMSHARE_METRIC_COSINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(DistSmem)) != cudaSuccess ||
         cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(kPlanSortCap * sizeof(unsigned long long))) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
@@ -875,7 +944,10 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   int64_t plan_np2 = 1;
   while (plan_np2 < target_cap && plan_np2 < kPlanSortCap) plan_np2 <<= 1;
   if (kAnchors > 1) plan_kernel<<<1, kPlanThreads, (size_t)plan_np2 * sizeof(unsigned long long), st>>>(a);
-  distance_kernel<<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
+  if (metric == MEMSHARE_METRIC_COSINE)
+    distance_kernel<MEMSHARE_METRIC_COSINE><<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
+  else
+    distance_kernel<MEMSHARE_METRIC_EUCLIDEAN><<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
   finalize_kernel<<<fin_grid, kConsumers, 0, st>>>(a, 0);
   return launch_status();
 }

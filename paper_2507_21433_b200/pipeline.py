@@ -99,7 +99,8 @@ class MemSharePath:
         self.decisions = e(caps.target * 32, torch.uint8)
         ws = max(L.segment_steps_workspace_size(self.num_tokens, self.num_seqs, caps.step),
                  L.step_candidates_workspace_size(self.num_tokens, self.num_seqs, caps.step, caps.match),
-                 L.block_distance_workspace_size(self.dims, self.num_blocks, caps.pair, caps.target),
+                 L.block_distance_workspace_size(self.dims, self.num_blocks, caps.pair, caps.target,
+                                                 L.METRIC_COSINE),
                  L.remap_workspace_size(self.num_blocks, caps.target))
         self.workspace = e(ws, torch.uint8)
 
@@ -126,12 +127,12 @@ class MemSharePath:
                                   self.num_pairs, self.target_off, self.caps.target, self.num_targets, self.workspace,
                                   self.status, self.stream), "step_candidates")
 
-    def distance_call(self, tau_b, mode=L.DIST_FULL, partial_sq=None):
+    def distance_call(self, tau_b, mode=L.DIST_FULL, partial_sq=None, metric=L.METRIC_EUCLIDEAN):
         ps = partial_sq if partial_sq is not None else self.partial_sq
         L.check(L.block_distance(None if mode == L.DIST_FINALIZE else self.pool, self.dims, self.pairs,
                                  self.target_off, self.num_pairs, self.num_targets, self.caps.pair, self.caps.target,
                                  mode, ps, tau_b, self.distance, self.under, self.decisions, self.workspace,
-                                 self.status, self.stream), "block_distance")
+                                 self.status, self.stream, metric), "block_distance")
 
     def remap(self):
         L.check(L.remap(self.table, self.table_stride, self.num_seqs, self.refcount, self.num_blocks, self.free_list,

@@ -69,6 +69,6 @@ def test_invalid_arguments_rejected_before_any_launch(lib):
     assert L.memshare_segment_steps(nul, 0, nul, nul, nul, 1, d, 1, nul, nul, nul, nul, 0, nul, 0, nul, nul) == 1
     assert L.memshare_segment_steps(nul, 0, nul, nul, nul, 1, d, 0, nul, nul, nul, nul, 0, nul, 0, nul, nul) == 1
     dims = lib.Dims(64, 8, 8, 12, 16)        # head_dim % 8 != 0
-    assert L.memshare_block_distance(nul, ctypes.byref(dims), nul, nul, nul, nul, 0, 0, 0, nul, 0.1, nul, nul, nul,
-                                     nul, 0, nul, nul) == 1
+    assert L.memshare_block_distance(nul, ctypes.byref(dims), nul, nul, nul, nul, 0, 0, 0, 0, nul, 0.1, nul, nul,
+                                     nul, nul, 0, nul, nul) == 1
     assert L.memshare_remap(nul, 0, 0, nul, 0, nul, nul, nul, nul, 0, 16, nul, nul, nul, 0, nul, nul) == 1

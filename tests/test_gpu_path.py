@@ -321,3 +321,61 @@ def test_c2_full_size_parity():
     assert oc["pairs"]["seq"].size > 150
     print(f"c2: pairs={oc['pairs']['seq'].size} targets={oc['target_off'].size - 1} near_thresh={near_thr} "
           f"near_tie={near_tie}")
+
+
+COS_ATOL = 2e-6      # fp32 dot/norm sums of <= 2^14 bf16 products, cosine formed in fp64 (R34)
+
+
+@pytest.mark.parametrize("shape,eta", [(SMALL, 0.05), (kv.QWEN32B, 0.02)])
+def test_cosine_metric_vs_oracle(shape, eta):
+    """f2: cosine block similarity D = 1 - mean_l (cos_K + cos_V)/2, GPU vs
+    the fp64 oracle on the same candidate pairs; argmin/threshold decisions equal wherever the
+    margins exceed the tolerance."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    w = workloads.small(shape, 2, 3100, seed=21, eta=eta)
+    p = make_path(w)
+    p.autosize(w.tau_s)
+    p.segment()
+    p.candidates(w.tau_s)
+    tau_b = 1.6 * eta * eta      # duplicate pair: both blocks carry independent noise -> D ~ eta^2
+    p.distance_call(tau_b, L.DIST_FULL, metric=L.METRIC_COSINE)
+    torch.cuda.synchronize()
+    assert p.status.item() == 0
+    got = p.read_distance()
+    oc = p.read_candidates()["pairs"]
+    assert oc["target_phys"].size > 50
+    kh, vh = host_pool_from_device(p.k_pool, p.v_pool)
+    Do = oracle.block_cosine(kh, vh, p.pool.layer_stride, p.pool.block_stride, shape.num_layers,
+                             shape.num_kv_heads, shape.head_dim, shape.block_size, oc["target_phys"],
+                             oc["source_phys"])
+    Dg = got["distance"].astype(np.float64)
+    same = oc["target_phys"] == oc["source_phys"]
+    assert np.all(Dg[same] == 0.0)
+    err = np.abs(Dg - Do)
+    assert err.max() <= COS_ATOL, f"max abs err {err.max():.3e}"
+    toff = p.read_candidates()["target_off"]
+    best, acc, _ = oracle.select(Do, toff, oc["source_logical"], tau_b)
+    dec = got["decisions"]
+    checked = 0
+    for t in range(toff.size - 1):
+        Ds = np.sort(Do[toff[t]:toff[t + 1]])
+        clear_tie = Ds.size < 2 or Ds[1] - Ds[0] > 2 * COS_ATOL
+        if clear_tie:
+            assert dec["source_logical"][t] == oc["source_logical"][best[t]]
+        if abs(Do[best[t]] - tau_b) > 2 * COS_ATOL:
+            assert bool(dec["accepted"][t]) == bool(acc[t])
+            checked += 1
+    assert checked > 0 and acc.any() and not acc.all()
+
+
+def test_cosine_metric_rejects_partial_modes():
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    w = workloads.small(SMALL, 2, 2000, seed=4)
+    p = make_path(w)
+    p.autosize(w.tau_s)
+    p.alloc_partial()
+    with pytest.raises(RuntimeError):
+        p.distance_call(0.01, L.DIST_PARTIAL, metric=L.METRIC_COSINE)
+    torch.cuda.synchronize()

@@ -192,3 +192,31 @@ def test_select_argmin_ties_and_strict_threshold():
     assert best.tolist() == [2, 3, 5]            # tie 0.1/0.1 -> smaller source logical 4; tie 0.25 -> logical 2
     assert acc.tolist() == [1, 0, 0]             # 0.25 is not < 0.25 (strict, reading R21)
     assert under.tolist() == [0, 1, 1, 0, 0, 0]
+
+
+# ------------------------------------------------------------------- f2: cosine block metric
+def test_cosine_metric_pins():
+    """cosine measures only angular alignment. Identical -> 0; a scaled copy
+    (x2, bf16-exact) -> 0 (magnitude ignored, unlike Alg. 1's D); negated -> 2; orthogonal -> 1."""
+    rng = np.random.default_rng(5)
+    sl = 2 * 2 * 8
+    base = (rng.integers(-8, 8, (1, 1, sl)) * 0.25).astype(np.float32)
+    orth = np.zeros_like(base)
+    half = sl // 2
+    b1 = base.copy(); b1[..., half:] = 0
+    orth[..., half:] = 1.0                                  # disjoint supports -> dot 0
+    vals = np.concatenate([b1, b1, 2 * b1, -b1, orth], axis=1)
+    k, v, ls, bs = pool_from_values(vals, vals)
+    D = oracle.block_cosine(k, v, ls, bs, 1, 2, 8, 2, [0, 0, 0, 0], [1, 2, 3, 4])
+    assert D[0] == 0.0 and abs(D[1]) < 1e-15 and abs(D[2] - 2.0) < 1e-15 and D[3] == 1.0
+    # against numpy on random blocks
+    k2, v2, ls2, bs2, nbk = _tiny_pool()
+    f = lambda a: (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    K = f(k2).reshape(2, nbk, -1)
+    V = f(v2).reshape(2, nbk, -1)
+    i, j = np.arange(0, 10), np.arange(10, 20)
+    cos = lambda A, B: (A * B).sum(-1) / np.sqrt((A * A).sum(-1) * (B * B).sum(-1))
+    ref = 1 - np.mean([(cos(K[l, i], K[l, j]) + cos(V[l, i], V[l, j])) / 2 for l in range(2)], axis=0)
+    got = oracle.block_cosine(k2, v2, ls2, bs2, 2, 2, 64, 16, i, j)
+    assert np.allclose(got, ref, rtol=0, atol=1e-13)
+    assert np.array_equal(got, oracle.block_cosine(k2, v2, ls2, bs2, 2, 2, 64, 16, j, i))
