@@ -424,7 +424,8 @@ def main():
             return 1e3 * o0.elapsed_time(o1) / n_on, o_pairs, n_on
 
         last_us, last_pairs, n_on = time_round(L.CUR_LAST)
-        busy_us, busy_pairs, _ = time_round(L.CUR_RANGE, busiest, busiest + 1)
+        bb = torch.as_tensor(busiest, device=dev)
+        busy_us, busy_pairs, _ = time_round(L.CUR_RANGE, bb, bb + 1)
         online = {"round_us": last_us, "pairs_per_round": last_pairs,
                   "busiest_round_us": busy_us, "busiest_pairs_per_round": busy_pairs,
                   "current_steps_per_round": w.batch.num_seqs, "rounds": n_on,

@@ -130,7 +130,7 @@ typedef struct memshare_decision {
  * to the step it ends), or at the last token of a FINAL sequence; tokens before gen_start[s]
  * are the prompt. Only finished steps are emitted; an open tail is not a step (reading R3).
  *   tokens        int32 [num_tokens]             concatenated token ids of all sequences
- *   num_tokens    host int64 == seq_tok_off[num_seqs] (< 2^31; sizes the tile grid)
+ *   num_tokens    host int64 == seq_tok_off[num_seqs] (< 2^31 - 4096; sizes the tile grid)
  *   seq_tok_off   int64 [num_seqs+1]             sequence s = tokens[seq_tok_off[s] .. [s+1]),
  *                                                non-decreasing, seq_tok_off[0] = 0
  *   gen_start     int32 [num_seqs]               first generated position of each sequence
@@ -141,8 +141,9 @@ typedef struct memshare_decision {
  *   step_nbag     int32 [step_cap]               content (non-delimiter) tokens of the step
  *   seq_step_off  int64 [num_seqs+1]             always written in full (the required size is
  *                                                seq_step_off[num_seqs]; CAPACITY if > step_cap)
- * Implementation: tile-parallel over the flat token array (4096 tokens per CTA) with a
- * device-wide scan of step ends, so one long sequence spreads over many SMs.
+ * Implementation: one single-pass kernel, tile-parallel over the flat token array (4096 tokens
+ * per CTA) with a decoupled look-back scan of (step ends, content tokens, last step boundary),
+ * so one long sequence spreads over many SMs (plus one memset of the per-tile flags).
  * Errors: INVALID_ARGUMENT for null pointers, num_seqs < 0, num_delims outside 1..16, step_cap
  * < 0, a short workspace. */
 memshare_status memshare_segment_steps(const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off,

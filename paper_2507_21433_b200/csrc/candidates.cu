@@ -179,6 +179,10 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   extern __shared__ int2 s_tab[];                         // [kSmemSlots]
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
+    *a.ws.done = 0u;
+    *a.ws.stash_alloc = 0ull;
+  }
   for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
     const int32_t s = seq_of_step(a, g);
     const int64_t tok_base = a.seq_tok_off[s];
@@ -712,9 +716,6 @@ extern "C" memshare_status memshare_step_candidates(
     cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FillSmem));
     attr_set = true;
   }
-  // done counter + stash allocator (adjacent, first two allocations)
-  if (cudaMemsetAsync(a.ws.done, 0, 256, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
-  if (cudaMemsetAsync(a.ws.stash_alloc, 0, sizeof(unsigned long long), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   const int sms = sm_count();
   const int64_t gcap = step_cap < 1 ? 1 : step_cap;
   const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);

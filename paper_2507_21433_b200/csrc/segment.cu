@@ -1,15 +1,15 @@
 // a1 -- step segmentation (readings R1-R4).
 //
-// Tile-parallel over the FLAT token array (sequences are concatenated, so the global order of
-// step ends is the global step order and a device-wide scan numbers them directly):
-//   seg_count : one CTA per 4096-token tile counts step ends and in-generation content tokens;
-//               the last CTA scans the tile counts into tile offsets (and writes the
-//               seq_step_off entries of trailing empty sequences and the total).
-//   seg_fill  : each tile re-derives its flags, block-scans them and writes, per step end,
-//               step_end and the inclusive content prefix; the thread holding a sequence's
-//               first token writes seq_step_off[s] and the content count before s.
-//   seg_final : one thread per step: step_start = previous end in the sequence (or gen_start),
-//               content count = prefix difference.
+// ONE single-pass kernel over the FLAT token array (sequences are concatenated, so the global
+// order of step ends is the global step order). Each CTA owns a 4096-token tile and computes,
+// per thread of 4 tokens, an aggregate (ends, content, last boundary): a "boundary" is the
+// position where the next step starts -- a sequence's generation start, or the token after a
+// step end -- together with the content-token prefix at that point. Aggregates combine with an
+// associative operator (counts add; the later boundary wins), so a block scan gives each
+// thread its prefix within the tile and a decoupled look-back over the preceding tiles' published
+// aggregates / inclusive prefixes gives the tile's prefix. Every step end then knows its global
+// step number (ends before it), its start (the last boundary) and its bag size (content since
+// that boundary) without a second pass.
 // A token i of sequence s (local position q, length n) ends a step iff q >= gen_start and
 //   (q + 1 < n) ? (t[i] in D && t[i+1] not in D) : final[s]          (reading R3).
 #include <climits>
@@ -23,24 +23,46 @@ constexpr int kNT = 1024;
 constexpr int kItems = 4;
 constexpr int kTile = kNT * kItems;
 
-struct SegWs {
-  int64_t* tile_cnt;    // [tiles] packed (ends << 32 | content)
-  int64_t* tile_off;    // [tiles + 1] exclusive, packed
-  int32_t* step_seq;    // [step_cap]
-  int64_t* cum;         // [step_cap] inclusive content prefix at each step end
-  int64_t* seq_cbase;   // [num_seqs + 1] content tokens before sequence s
-  unsigned int* done;
+// (ends, content, bpos, bcb): bpos = position (flat) of the last boundary or -1, bcb = content
+// tokens before bpos counted from the start of the range the aggregate covers.
+struct Agg {
+  int32_t e, c, bpos, bcb;
 };
 
-SegWs seg_layout(Ws& w, int64_t num_tokens, int32_t num_seqs, int64_t step_cap) {
+__device__ __forceinline__ Agg agg_identity() { return Agg{0, 0, -1, 0}; }
+
+// a (earlier range) then b (later range)
+__device__ __forceinline__ Agg combine(const Agg& a, const Agg& b) {
+  Agg r;
+  r.e = a.e + b.e;
+  r.c = a.c + b.c;
+  if (b.bpos >= 0) { r.bpos = b.bpos; r.bcb = a.c + b.bcb; }
+  else { r.bpos = a.bpos; r.bcb = a.bcb; }
+  return r;
+}
+
+__device__ __forceinline__ Agg shfl_agg_up(const Agg& v, int o) {
+  return Agg{__shfl_up_sync(0xffffffffu, v.e, o), __shfl_up_sync(0xffffffffu, v.c, o),
+             __shfl_up_sync(0xffffffffu, v.bpos, o), __shfl_up_sync(0xffffffffu, v.bcb, o)};
+}
+
+__device__ __forceinline__ Agg shfl_agg_down(const Agg& v, int o) {
+  return Agg{__shfl_down_sync(0xffffffffu, v.e, o), __shfl_down_sync(0xffffffffu, v.c, o),
+             __shfl_down_sync(0xffffffffu, v.bpos, o), __shfl_down_sync(0xffffffffu, v.bcb, o)};
+}
+
+struct SegWs {
+  int32_t* flag;   // [tiles] 0 = nothing, 1 = aggregate, 2 = inclusive prefix (zeroed per call)
+  int4* agg;       // [tiles]
+  int4* inc;       // [tiles]
+};
+
+SegWs seg_layout(Ws& w, int64_t num_tokens) {
   const int64_t tiles = (num_tokens + kTile - 1) / kTile;
   SegWs s;
-  s.tile_cnt = w.take<int64_t>(tiles + 1);
-  s.tile_off = w.take<int64_t>(tiles + 2);
-  s.step_seq = w.take<int32_t>(step_cap + 1);
-  s.cum = w.take<int64_t>(step_cap + 1);
-  s.seq_cbase = w.take<int64_t>((size_t)num_seqs + 1);
-  s.done = w.take<unsigned int>(1);
+  s.flag = w.take<int32_t>(tiles + 1);
+  s.agg = w.take<int4>(tiles + 1);
+  s.inc = w.take<int4>(tiles + 1);
   return s;
 }
 
@@ -71,126 +93,214 @@ __device__ __forceinline__ int32_t seq_of_token(const SegArgs& a, int64_t i) {
   return lo;
 }
 
-struct TokFlags {
-  uint32_t end, content;
-  int32_t seq0;            // sequence of the thread's first token
+// the sequence context of a flat position (advanced monotonically)
+struct SeqCur {
+  int32_t s;
+  int64_t off, nxt, gs;
+  bool fin;
 };
 
-// flags of the kItems tokens starting at global position i0
-__device__ __forceinline__ TokFlags token_flags(const SegArgs& a, int64_t i0) {
-  TokFlags f{0u, 0u, 0};
-  if (i0 >= a.num_tokens) return f;
-  int32_t s = seq_of_token(a, i0);
-  f.seq0 = s;
-  int64_t off = __ldg(a.seq_tok_off + s), nxt = __ldg(a.seq_tok_off + s + 1);
-  int64_t gs = off + (int64_t)max(0, __ldg(a.gen_start + s));
-  bool fin = __ldg(a.seq_final + s) != 0;
-  bool dcur = is_delim(a.tokens[i0], a.dl);
+__device__ __forceinline__ void seq_load(const SegArgs& a, SeqCur& q, int32_t s) {
+  q.s = s;
+  q.off = __ldg(a.seq_tok_off + s);
+  q.nxt = __ldg(a.seq_tok_off + s + 1);
+  const int64_t n = q.nxt - q.off;
+  const int32_t g = __ldg(a.gen_start + s);
+  q.gs = q.off + (g < 0 ? 0 : (g > n ? n : (int64_t)g));
+  q.fin = __ldg(a.seq_final + s) != 0;
+}
+
+__device__ __forceinline__ void seq_advance(const SegArgs& a, SeqCur& q, int64_t i) {
+  while (i >= q.nxt) seq_load(a, q, q.s + 1);   // crossed into the next (non-empty) sequence
+}
+
+struct Bits {
+  uint32_t end, content, gstart;
+};
+
+// flags of the kItems tokens starting at i0 (i0 < num_tokens)
+__device__ __forceinline__ Bits token_bits(const SegArgs& a, int64_t i0, SeqCur& q) {
+  Bits b{0u, 0u, 0u};
+  int32_t tk[kItems + 1];
+#pragma unroll
+  for (int j = 0; j <= kItems; ++j) tk[j] = (i0 + j < a.num_tokens) ? __ldg(a.tokens + i0 + j) : INT_MIN;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const int64_t i = i0 + j;
     if (i >= a.num_tokens) break;
-    while (i >= nxt) {                        // crossed into the next (non-empty) sequence
-      ++s;
-      off = nxt;
-      nxt = __ldg(a.seq_tok_off + s + 1);
-      gs = off + (int64_t)max(0, __ldg(a.gen_start + s));
-      fin = __ldg(a.seq_final + s) != 0;
+    seq_advance(a, q, i);
+    if (i >= q.gs) {
+      const bool dcur = is_delim(tk[j], a.dl);
+      const bool e = (i + 1 < q.nxt) ? (dcur && !is_delim(tk[j + 1], a.dl)) : q.fin;
+      b.end |= (e ? 1u : 0u) << j;
+      b.content |= (dcur ? 0u : 1u) << j;
+      b.gstart |= (i == q.gs ? 1u : 0u) << j;
     }
-    const bool dnext = (i + 1 < nxt) ? is_delim(a.tokens[i + 1], a.dl) : false;
-    if (i >= gs) {
-      const bool e = (i + 1 < nxt) ? (dcur && !dnext) : fin;
-      f.end |= (e ? 1u : 0u) << j;
-      f.content |= (dcur ? 0u : 1u) << j;
-    }
-    dcur = (i + 1 < a.num_tokens) ? ((i + 1 < nxt) ? dnext : is_delim(a.tokens[i + 1], a.dl)) : false;
   }
-  return f;
+  return b;
 }
 
-__global__ void __launch_bounds__(kNT) seg_count_kernel(SegArgs a) {
-  __shared__ int64_t sh[kNT / 32 + 1];
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ Agg ld_agg(const int4* p) {
+  const int4 v = __ldcg(p);
+  return Agg{v.x, v.y, v.z, v.w};
+}
+
+__global__ void __launch_bounds__(kNT) seg_kernel(SegArgs a) {
+  __shared__ Agg s_warp[kNT / 32];
+  __shared__ Agg s_tile_prefix;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t tiles = (a.num_tokens + kTile - 1) / kTile;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const TokFlags f = token_flags(a, tile * kTile + (int64_t)threadIdx.x * kItems);
-    const int64_t packed = ((int64_t)__popc(f.end) << 32) | (int64_t)__popc(f.content);
-    const int64_t tot = block_sum<kNT>(packed, sh);
-    if (threadIdx.x == 0) a.ws.tile_cnt[tile] = tot;
+  const int64_t tile = blockIdx.x;
+  if (tiles == 0) {                                      // no tokens: every sequence has 0 steps
+    for (int32_t s = threadIdx.x; s <= a.num_seqs; s += kNT) a.seq_step_off[s] = 0;
+    return;
   }
-  if (last_block_done(a.ws.done)) {
-    int64_t carry = 0;
-    for (int64_t base = 0; base < tiles; base += kNT) {
-      const int64_t i = base + threadIdx.x;
-      const int64_t v = i < tiles ? __ldcg(a.ws.tile_cnt + i) : 0;
-      int64_t tot;
-      const int64_t ex = block_excl_scan<kNT>(v, tot, sh);
-      if (i < tiles) a.ws.tile_off[i] = carry + ex;
-      carry += tot;
+  const int64_t i0 = tile * kTile + (int64_t)threadIdx.x * kItems;
+  const bool live = i0 < a.num_tokens;
+  SeqCur q{};
+  Bits b{0u, 0u, 0u};
+  if (live) {
+    seq_load(a, q, seq_of_token(a, i0));
+    b = token_bits(a, i0, q);
+  }
+  // thread aggregate
+  Agg mine = agg_identity();
+  mine.e = __popc(b.end);
+  mine.c = __popc(b.content);
+  {
+    int32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      if ((b.gstart >> j) & 1u) { mine.bpos = (int32_t)(i0 + j); mine.bcb = c; }
+      c += (b.content >> j) & 1u;
+      if ((b.end >> j) & 1u) { mine.bpos = (int32_t)(i0 + j + 1); mine.bcb = c; }
     }
-    if (threadIdx.x == 0) {
-      a.ws.tile_off[tiles] = carry;
-      const int64_t total = carry >> 32;
-      if (total > a.step_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+  }
+  // block-wide exclusive scan of the thread aggregates
+  Agg x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Agg y = shfl_agg_up(x, o);
+    if (lane >= o) x = combine(y, x);
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    Agg v = s_warp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const Agg y = shfl_agg_up(v, o);
+      if (lane >= o) v = combine(y, v);
     }
-    // sequences that start at the end of the token array (trailing empties) and the total
-    for (int32_t s = threadIdx.x; s <= a.num_seqs; s += kNT) {
-      if (__ldg(a.seq_tok_off + s) >= a.num_tokens) {
-        a.seq_step_off[s] = carry >> 32;
-        a.ws.seq_cbase[s] = carry & 0xffffffffll;
+    s_warp[lane] = v;                                    // inclusive warp totals
+  }
+  __syncthreads();
+  Agg excl = shfl_agg_up(x, 1);
+  if (lane == 0) excl = agg_identity();
+  if (w > 0) excl = combine(s_warp[w - 1], excl);
+  const Agg tile_agg = s_warp[kNT / 32 - 1];
+  // decoupled look-back for the tile prefix
+  if (w == 0) {
+    if (tile == 0) {
+      if (lane == 0) {
+        a.ws.inc[0] = make_int4(tile_agg.e, tile_agg.c, tile_agg.bpos, tile_agg.bcb);
+        __threadfence();
+        st_release(a.ws.flag, 2);
+        s_tile_prefix = agg_identity();
+      }
+    } else {
+      if (lane == 0) {
+        a.ws.agg[tile] = make_int4(tile_agg.e, tile_agg.c, tile_agg.bpos, tile_agg.bcb);
+        __threadfence();
+        st_release(a.ws.flag + tile, 1);
+      }
+      Agg run = agg_identity();                          // combination of tiles (p, tile)
+      int64_t p = tile - 1;
+      for (;;) {
+        const int64_t qi = p - lane;
+        int32_t f = 2;
+        if (qi >= 0) {
+          while ((f = ld_acquire(a.ws.flag + qi)) == 0) {
+          }
+        }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = inc_mask ? __ffs(inc_mask) - 1 : 32;   // lowest lane (latest tile) with a prefix
+        Agg v = agg_identity();
+        if (lane < stop && qi >= 0) v = ld_agg(a.ws.agg + qi);
+        else if (lane == stop && qi >= 0) v = ld_agg(a.ws.inc + qi);
+        // ordered reduction: higher lane = earlier tile
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const Agg y = shfl_agg_down(v, o);
+          if (lane + o < 32) v = combine(y, v);
+        }
+        v.e = __shfl_sync(0xffffffffu, v.e, 0);
+        v.c = __shfl_sync(0xffffffffu, v.c, 0);
+        v.bpos = __shfl_sync(0xffffffffu, v.bpos, 0);
+        v.bcb = __shfl_sync(0xffffffffu, v.bcb, 0);
+        run = combine(v, run);
+        if (stop < 32) break;
+        p -= 32;
+      }
+      if (lane == 0) {
+        const Agg incl = combine(run, tile_agg);
+        a.ws.inc[tile] = make_int4(incl.e, incl.c, incl.bpos, incl.bcb);
+        __threadfence();
+        st_release(a.ws.flag + tile, 2);
+        s_tile_prefix = run;
       }
     }
   }
-}
-
-__global__ void __launch_bounds__(kNT) seg_fill_kernel(SegArgs a) {
-  __shared__ int64_t sh[kNT / 32 + 1];
-  const int64_t tiles = (a.num_tokens + kTile - 1) / kTile;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t i0 = tile * kTile + (int64_t)threadIdx.x * kItems;
-    const TokFlags f = token_flags(a, i0);
-    const int64_t packed = ((int64_t)__popc(f.end) << 32) | (int64_t)__popc(f.content);
-    int64_t tot;
-    const int64_t ex = block_excl_scan<kNT>(packed, tot, sh) + __ldcg(a.ws.tile_off + tile);
-    int64_t m = ex >> 32, c = ex & 0xffffffffll;
-    int32_t s = f.seq0;
+  __syncthreads();
+  const Agg tp = s_tile_prefix;
+  if (live) {
+    const Agg pre = combine(tp, excl);                   // everything before this thread's tokens
+    int64_t m = pre.e;
+    int32_t c = pre.c;
+    int64_t bpos = pre.bpos;
+    int32_t bcb = pre.bcb;
+    seq_load(a, q, seq_of_token(a, i0));
+#pragma unroll
     for (int j = 0; j < kItems; ++j) {
       const int64_t i = i0 + j;
       if (i >= a.num_tokens) break;
-      while (i >= __ldg(a.seq_tok_off + s + 1)) ++s;
-      const int64_t off = __ldg(a.seq_tok_off + s);
-      if (i == off) {
+      seq_advance(a, q, i);
+      if (i == q.off) {
         // first token of s (and of the empty sequences just before it sharing this offset)
-        int32_t s0 = s;
-        while (s0 > 0 && __ldg(a.seq_tok_off + s0 - 1) == off) --s0;
-        for (int32_t q = s0; q <= s; ++q) {
-          a.seq_step_off[q] = m;
-          a.ws.seq_cbase[q] = c;
-        }
+        int32_t s0 = q.s;
+        while (s0 > 0 && __ldg(a.seq_tok_off + s0 - 1) == q.off) --s0;
+        for (int32_t r = s0; r <= q.s; ++r) a.seq_step_off[r] = m;
       }
-      c += (f.content >> j) & 1u;
-      if ((f.end >> j) & 1u) {
+      if ((b.gstart >> j) & 1u) { bpos = i; bcb = c; }
+      c += (b.content >> j) & 1u;
+      if ((b.end >> j) & 1u) {
         if (m < a.step_cap) {
-          a.step_end[m] = (int32_t)(i - off + 1);
-          a.ws.step_seq[m] = s;
-          a.ws.cum[m] = c;
+          a.step_end[m] = (int32_t)(i - q.off + 1);
+          a.step_start[m] = (int32_t)(bpos - q.off);
+          a.step_nbag[m] = c - bcb;
         }
         ++m;
+        bpos = i + 1;
+        bcb = c;
       }
     }
   }
-}
-
-__global__ void seg_final_kernel(SegArgs a) {
-  int64_t G = __ldcg(a.seq_step_off + a.num_seqs);
-  G = G < a.step_cap ? G : a.step_cap;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = a.ws.step_seq[g];
-    const bool first = g == a.seq_step_off[s];
-    const int64_t n = a.seq_tok_off[s + 1] - a.seq_tok_off[s];
-    const int32_t gsv = a.gen_start[s];
-    const int64_t gs = gsv < 0 ? 0 : (gsv > n ? n : gsv);
-    a.step_start[g] = first ? (int32_t)gs : a.step_end[g - 1];
-    a.step_nbag[g] = (int32_t)(a.ws.cum[g] - (first ? a.ws.seq_cbase[s] : a.ws.cum[g - 1]));
+  if (tile == tiles - 1) {
+    const int64_t total = (int64_t)tp.e + tile_agg.e;
+    if (threadIdx.x == 0 && total > a.step_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+    // sequences that start at the end of the token array (trailing empties) and the total
+    for (int32_t s = threadIdx.x; s <= a.num_seqs; s += kNT)
+      if (__ldg(a.seq_tok_off + s) >= a.num_tokens) a.seq_step_off[s] = total;
   }
 }
 
@@ -202,7 +312,7 @@ using namespace ms;
 extern "C" size_t memshare_segment_steps_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap) {
   if (num_tokens < 0 || num_seqs < 0 || step_cap < 0) return 0;
   Ws w{nullptr, 0};
-  seg_layout(w, num_tokens, num_seqs, step_cap);
+  seg_layout(w, num_tokens);
   return w.size();
 }
 
@@ -212,7 +322,7 @@ extern "C" memshare_status memshare_segment_steps(const int32_t* tokens, int64_t
                                                   int32_t* step_start, int32_t* step_end, int32_t* step_nbag,
                                                   int64_t* seq_step_off, int64_t step_cap, void* workspace,
                                                   size_t workspace_bytes, int32_t* device_status, void* stream) {
-  if (num_tokens < 0 || num_tokens > (int64_t)INT32_MAX || num_seqs < 0 || step_cap < 0 || num_delims < 1 ||
+  if (num_tokens < 0 || num_tokens > (int64_t)INT32_MAX - kTile || num_seqs < 0 || step_cap < 0 || num_delims < 1 ||
       num_delims > MEMSHARE_MAX_DELIMS)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (!seq_tok_off || !seq_step_off || !delim_ids_host || !workspace || !device_status) return MEMSHARE_ERR_INVALID_ARGUMENT;
@@ -229,15 +339,11 @@ extern "C" memshare_status memshare_segment_steps(const int32_t* tokens, int64_t
   a.step_start = step_start; a.step_end = step_end; a.step_nbag = step_nbag; a.seq_step_off = seq_step_off;
   a.step_cap = step_cap; a.status = device_status;
   Ws w{static_cast<char*>(workspace), 0};
-  a.ws = seg_layout(w, num_tokens, num_seqs, step_cap);
+  a.ws = seg_layout(w, num_tokens);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(a.ws.done, 0, sizeof(unsigned int), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   const int64_t tiles = (num_tokens + kTile - 1) / kTile;
-  const int grid = (int)(tiles < 1 ? 1 : (tiles < 4 * sm_count() ? tiles : 4 * sm_count()));
-  seg_count_kernel<<<grid, kNT, 0, st>>>(a);
-  seg_fill_kernel<<<grid, kNT, 0, st>>>(a);
-  const int64_t sc = step_cap < 1 ? 1 : step_cap;
-  const int fgrid = (int)((sc + 255) / 256 < 4 * sm_count() ? (sc + 255) / 256 : 4 * sm_count());
-  seg_final_kernel<<<fgrid, 256, 0, st>>>(a);
+  if (tiles > 0 && cudaMemsetAsync(a.ws.flag, 0, (size_t)tiles * sizeof(int32_t), st) != cudaSuccess)
+    return MEMSHARE_ERR_CUDA;
+  seg_kernel<<<(unsigned)(tiles < 1 ? 1 : tiles), kNT, 0, st>>>(a);
   return launch_status();
 }

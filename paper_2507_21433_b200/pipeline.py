@@ -27,6 +27,9 @@ class Caps:
 
 
 def _dev_i32(a, dev):
+    """int32 device tensor; a device int32 tensor passes through (usable inside graph capture)."""
+    if isinstance(a, torch.Tensor) and a.device.type == dev.type and a.dtype == torch.int32:
+        return a.contiguous()
     return torch.as_tensor(np.ascontiguousarray(a, np.int32), device=dev)
 
 

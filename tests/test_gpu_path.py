@@ -379,3 +379,37 @@ def test_cosine_metric_rejects_partial_modes():
     with pytest.raises(RuntimeError):
         p.distance_call(0.01, L.DIST_PARTIAL, metric=L.METRIC_COSINE)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_segment_many_tiles(seed):
+    """> 32 tiles (several look-back windows of the single-pass scan), empty and one-token
+    sequences between long ones, mixed final flags and prompt lengths, steps crossing tiles."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    rng = np.random.default_rng(100 + seed)
+    lens = rng.choice([0, 1, 7, 3000, 40000, 90000], 24, p=[0.15, 0.1, 0.15, 0.3, 0.2, 0.1])
+    seqs = [rng.choice([1, 2, 5, 6, 7, 8], n, p=[0.03, 0.01, 0.24, 0.24, 0.24, 0.24]).astype(np.int32) for n in lens]
+    toks = np.concatenate(seqs).astype(np.int32)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    gs = np.minimum(rng.integers(0, 300, lens.size), np.maximum(lens, 0) + 2).astype(np.int32)
+    fin = rng.integers(0, 2, lens.size).astype(np.uint8)
+    delims = np.asarray([1, 2], np.int32)
+    exp = oracle.segment_steps(toks, off, gs, fin, delims)
+    assert toks.size > 33 * 4096
+    dev = torch.device("cuda")
+    S, cap = lens.size, int(exp["seq_step_off"][-1]) + 5
+    out = [torch.full((cap,), -7, dtype=torch.int32, device=dev) for _ in range(3)]
+    sso = torch.full((S + 1,), -9, dtype=torch.int64, device=dev)
+    ws = torch.full((L.segment_steps_workspace_size(toks.size, S, cap),), 0xAB, dtype=torch.uint8, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    t = lambda a, dt: torch.as_tensor(a, dtype=dt, device=dev)
+    for _ in range(2):                                   # the second call reuses the dirty workspace
+        assert L.segment_steps(t(toks, torch.int32), toks.size, t(off, torch.int64), t(gs, torch.int32),
+                               t(fin, torch.uint8), S, delims, out[0], out[1], out[2], sso, cap, ws, status) == 0
+        torch.cuda.synchronize()
+        n = int(sso[-1])
+        assert status.item() == 0
+        got = {"step_start": out[0][:n].cpu().numpy(), "step_end": out[1][:n].cpu().numpy(),
+               "step_nbag": out[2][:n].cpu().numpy(), "seq_step_off": sso.cpu().numpy()}
+        assert_steps_equal(got, exp)
