@@ -6,9 +6,9 @@
 // earlier step j is  <c_k, c_j> = sum over content tokens p of j of c_k[t_p],  so only the
 // CURRENT step needs a count table: an open-addressing hash table in shared memory (global
 // workspace for steps > 2048 content tokens). Because steps tile the sequence, the whole
-// history of k is one contiguous token range; all threads stream it coalesced, probe k's table
-// and add hits to the dot product of the step holding the token (smem 64-bit atomics, located
-// by binary search over the staged step starts). Integer dot and norms are exact; the cosine is
+// history of k is one contiguous token range; the CTA stages it in shared memory with coalesced
+// loads, each thread walks a contiguous run, probes k's table and adds its partial dot once per
+// history step it touches (32-bit smem atomics with carry; step boundaries staged in smem). Integer dot and norms are exact; the cosine is
 // one IEEE expression (__ddiv_rn / __dsqrt_rn / __dmul_rn), bit-identical to the C oracle.
 //
 // Three launches:
@@ -34,6 +34,7 @@ constexpr int kSmemSlots = 8192;       // smem hash table (steps with <= 2048 co
 constexpr int kCandCap = 1024;         // survivors held per current step
 constexpr int kChunk = kCandCap / 2;   // history steps per selection chunk
 constexpr int kMaxTgt = 4096;          // full blocks per step handled by the fill kernel
+constexpr int kHistTok = 12288;        // history tokens staged in smem per pass (48 KiB)
 constexpr int32_t kEmpty = -1;
 
 struct CandWs {
@@ -50,7 +51,6 @@ struct CandWs {
   int64_t* off_p;
   double* stash_cos;     // [match_cap]
   int32_t* stash_j;
-  int32_t* tok_step;     // [num_tokens] global step of each token inside a finished step
   int2* gtab;            // [4*num_tokens] {key, count} global tables of oversize steps
 };
 
@@ -69,7 +69,6 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   c.off_p = w.take<int64_t>(step_cap + 1);
   c.stash_cos = w.take<double>(match_cap + 1);
   c.stash_j = w.take<int32_t>(match_cap + 1);
-  c.tok_step = w.take<int32_t>(num_tokens + 1);
   c.gtab = w.take<int2>(4 * num_tokens + 1);
   return c;
 }
@@ -187,7 +186,6 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
     const int32_t s = seq_of_step(a, g);
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t nbag = a.step_nbag[g];
-    for (int32_t p = a.step_start[g] + threadIdx.x; p < a.step_end[g]; p += kNT) a.ws.tok_step[tok_base + p] = (int32_t)g;
     int64_t n2 = 0;
     if (nbag > 0) {
       const Table tb = build_table(a, s_tab, a.tokens + tok_base, tok_base, a.step_start[g], a.step_end[g], nbag);
@@ -370,6 +368,7 @@ struct SelSmem {
   int32_t cum[kCandCap + 1];
   int32_t hst[kChunk];
   int32_t hen[kChunk];
+  int32_t tok[kHistTok];   // staged history tokens
   uint32_t dot_lo[kChunk];
   uint32_t dot_hi[kChunk];
   int64_t sh[kNW1 + 1];
@@ -379,25 +378,30 @@ struct SelSmem {
   uint32_t acc_p;
 };
 
+// Stream the history token range [clo, chi) (staged in shared memory at s_tok) through k's
+// count table. Each thread takes a contiguous run, walks the step boundaries (hen, smem) and
+// adds its partial dot once per step it touches. A rolled loop on purpose: this code runs once
+// per launch, so instruction-fetch misses of an unrolled body cost more than the work.
 template <bool kGlobal>
 __device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, uint32_t shift, uint32_t* dot_lo,
-                                               uint32_t* dot_hi, const int32_t* hen, int32_t d0, int32_t dn,
-                                               const Delims& dl, const int32_t* __restrict__ t,
-                                               const int32_t* __restrict__ ts, int32_t lo, int32_t hi, int64_t gjb,
-                                               bool dbg_noprobe) {
-  const int32_t n = hi - lo;
+                                               uint32_t* dot_hi, const int32_t* hen, int32_t nj, int32_t d0,
+                                               int32_t dn, const Delims& dl, const int32_t* s_tok, int32_t clo,
+                                               int32_t chi, bool dbg_noprobe) {
+  const int32_t n = chi - clo;
   const int32_t per = (n + kNT1 - 1) / kNT1;                // tokens per thread
-  int32_t p = lo + (int32_t)threadIdx.x * per;
-  const int32_t pe = (p + per < hi) ? p + per : hi;
+  int32_t p = clo + (int32_t)threadIdx.x * per;
+  const int32_t pe = (p + per < chi) ? p + per : chi;
   if (p >= pe) return;
-  int32_t jl = (int32_t)(__ldg(ts + p) - gjb);
+  int32_t jl = 0, jh = nj - 1;                              // first step with hen > p
+  while (jl < jh) {
+    const int32_t mid = (jl + jh) >> 1;
+    if (hen[mid] > p) jh = mid; else jl = mid + 1;
+  }
   int32_t bound = hen[jl];
   uint32_t acc = 0u;
-  int32_t nxt = __ldg(t + p);                               // software-pipelined token load
 #pragma unroll 1
   for (; p < pe; ++p) {
-    const int32_t tok = nxt;
-    if (p + 1 < pe) nxt = __ldg(t + p + 1);
+    const int32_t tok = s_tok[p - clo];
     if (p >= bound) {
       if (acc) { const uint32_t old = atomicAdd(dot_lo + jl, acc); if (old + acc < old) atomicAdd(dot_hi + jl, 1u); }
       acc = 0u;
@@ -417,6 +421,41 @@ __device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, u
     acc += (uint32_t)c;
   }
   if (acc) { const uint32_t old = atomicAdd(dot_lo + jl, acc); if (old + acc < old) atomicAdd(dot_hi + jl, 1u); }
+}
+
+// One-CTA exclusive scans of the per-step match / target / pair counts (one pass, one set of
+// barriers: the three int32 counts of a step travel packed as 3 x 21 bits when they fit).
+__device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
+  int64_t cm = 0, ct = 0, cp = 0;
+  for (int64_t base = 0; base < G; base += kNT1) {
+    const int64_t i = base + threadIdx.x;
+    int64_t m = 0, t = 0, p = 0;
+    if (i < G) { m = __ldcg(a.ws.cnt_m + i); t = __ldcg(a.ws.cnt_t + i); p = __ldcg(a.ws.cnt_p + i); }
+    int64_t tot;
+    // per-pass totals stay < 2^21 for each count when every step count is < 2^11 (1024 x 2047)
+    const bool packed = m < 2048 && t < 2048 && p < 2048;
+    const int all_packed = __syncthreads_and(packed);
+    if (all_packed) {
+      const int64_t ex = block_excl_scan<kNT1>(m | (t << 21) | (p << 42), tot, sh);
+      if (i < G) {
+        a.ws.off_m[i] = cm + (ex & 0x1FFFFF);
+        a.ws.off_t[i] = ct + ((ex >> 21) & 0x1FFFFF);
+        a.ws.off_p[i] = cp + (ex >> 42);
+      }
+      cm += tot & 0x1FFFFF; ct += (tot >> 21) & 0x1FFFFF; cp += tot >> 42;
+    } else {
+      const int64_t exm = block_excl_scan<kNT1>(m, tot, sh);
+      if (i < G) a.ws.off_m[i] = cm + exm;
+      cm += tot;
+      const int64_t ext = block_excl_scan<kNT1>(t, tot, sh);
+      if (i < G) a.ws.off_t[i] = ct + ext;
+      ct += tot;
+      const int64_t exp_ = block_excl_scan<kNT1>(p, tot, sh);
+      if (i < G) a.ws.off_p[i] = cp + exp_;
+      cp += tot;
+    }
+  }
+  if (threadIdx.x == 0) { a.ws.off_m[G] = cm; a.ws.off_t[G] = ct; a.ws.off_p[G] = cp; }
 }
 
 __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
@@ -458,18 +497,21 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       __syncthreads();
       if (jb == 0) DBG_T(10);
       const int32_t lo = sm.hst[0], hi = sm.hen[nj - 1];
-      const int32_t* ts = a.ws.tok_step + tok_base;
-      const int64_t gjb = gfirst + jb;
-      // each thread takes a contiguous run of tokens, walks the step boundaries in smem and adds
-      // its partial dot once per step it touches. A rolled loop on purpose: this code runs once
-      // per launch, so instruction-fetch misses of an unrolled body cost more than the loads.
-      if (!(a.dbg_skip & 1)) {
-        if (tb.global)
-          stream_history<true>(tb.slots, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, a.dl.id[0], a.dl.n, a.dl, t,
-                               ts, lo, hi, gjb, (a.dbg_skip & 16) != 0);
-        else
-          stream_history<false>(sm.tab, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, a.dl.id[0], a.dl.n, a.dl, t,
-                                ts, lo, hi, gjb, (a.dbg_skip & 16) != 0);
+      for (int32_t clo = lo; clo < hi; clo += kHistTok) {
+        const int32_t chi = (hi - clo > kHistTok) ? clo + kHistTok : hi;
+        // coalesced, independent loads: one memory latency for the whole pass
+#pragma unroll 4
+        for (int32_t i = threadIdx.x; i < chi - clo; i += kNT1) sm.tok[i] = __ldg(t + clo + i);
+        __syncthreads();
+        if (!(a.dbg_skip & 1)) {
+          if (tb.global)
+            stream_history<true>(tb.slots, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
+                                 a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
+          else
+            stream_history<false>(sm.tab, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
+                                  a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
+        }
+        __syncthreads();
       }
       __syncthreads();
       if (jb == 0) DBG_T(11);
@@ -545,9 +587,7 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
   DBG_T(7);
   if (!(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
     DBG_T(8);
-    cta_scan_counts<kNT1>(a.ws.cnt_m, a.ws.off_m, G, sm.sh);
-    cta_scan_counts<kNT1>(a.ws.cnt_t, a.ws.off_t, G, sm.sh);
-    cta_scan_counts<kNT1>(a.ws.cnt_p, a.ws.off_p, G, sm.sh);
+    scan_counts3(a, G, sm.sh);
     __syncthreads();
     if (threadIdx.x == 0) {
       const int64_t M = a.ws.off_m[G], T = a.ws.off_t[G], P = a.ws.off_p[G];

@@ -57,3 +57,23 @@ else:
     e.record()
     torch.cuda.synchronize()
     print(f"{'all':18s} {a.elapsed_time(e) / 500 * 1e3:7.1f} us / graph replay")
+
+if mode == "stamps":
+    # MEMSHARE_DEBUG_SKIP=8: phase stamps of stage1 in CUR_LAST mode (globaltimer ns)
+    import ctypes
+    for _ in range(50):
+        path.segment()
+        path.candidates(w.tau_s, cur_mode=L.CUR_LAST)
+    torch.cuda.synchronize()
+    buf = np.zeros(2048 * 16, np.uint64)
+    L.lib.memshare_debug_stage1_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    L.lib.memshare_debug_stage1_times(buf.ctypes.data, buf.size)
+    t = buf.reshape(2048, 16).astype(np.int64)[:148]
+    t0 = t[:, 0][t[:, 0] > 0].min()
+    G = int(path.seq_step_off[-1].item())
+    act = (G - 1) % 148
+    print("G", G, "active CTA", act)
+    print("active CTA stamps (us):", [(round((x - t0) / 1e3, 2) if x > 0 else None) for x in t[act, :12]])
+    print("CTA start spread (us):", (t[:, 0].max() - t0) / 1e3, " pre-last max:", (t[:, 7].max() - t0) / 1e3)
+    lastc = np.argmax(t[:, 8])
+    print("last CTA", lastc, "elected", (t[lastc, 8] - t0) / 1e3, "scans done", (t[lastc, 9] - t0) / 1e3)
