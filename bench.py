@@ -279,13 +279,12 @@ def main():
     if args.mode == "headshard":
         path.alloc_partial()
     torch.cuda.synchronize()
-    pristine = {n: getattr(path, n).clone() for n in ("table", "refcount", "free_list", "free_count")}
+    pristine = path.state.clone()
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
-    def restore():
-        for n, t in pristine.items():
-            getattr(path, n).copy_(t, non_blocking=True)
+    def restore():               # table + refcounts + free list + free count: one device copy
+        path.state.copy_(pristine, non_blocking=True)
 
     def front():                 # restore the round's initial state, a1, a2-a4
         restore()
@@ -336,7 +335,7 @@ def main():
     alg_bytes = kv_bytes + meta_bytes
 
     if args.breakdown:
-        calls = {"restore (torch copies)": restore, "segment_steps": path.segment,
+        calls = {"restore (state copy)": restore, "segment_steps": path.segment,
                  "step_candidates": lambda: path.candidates(w.tau_s),
                  "block_distance": lambda: path.distance_call(w.tau_b), "remap": path.remap}
         for name, fn in calls.items():
@@ -441,8 +440,9 @@ def main():
         pin = lambda x: torch.as_tensor(np.ascontiguousarray(x)).pin_memory()
         h_in = {"tokens": pin(b.tokens.astype(np.int32)), "seq_tok_off": pin(b.seq_tok_off.astype(np.int64)),
                 "gen_start": pin(b.gen_start.astype(np.int32)), "final": pin(b.final.astype(np.uint8)),
-                "table": pin(w.table.astype(np.int32).ravel()), "refcount": pin(w.refcount.astype(np.int32)),
-                "free_list": pin(w.free_list.astype(np.int32)), "free_count": pin(np.asarray([w.free_count], np.int64))}
+                "state": pin(np.concatenate([np.asarray([w.free_count], np.int64).view(np.int32),
+                                             w.table.astype(np.int32).ravel(), w.refcount.astype(np.int32),
+                                             w.free_list.astype(np.int32)]))}
         h2d = sum(x.numel() * x.element_size() for x in h_in.values())
         out_dec = torch.empty(path.decisions.numel(), dtype=torch.uint8).pin_memory()
         out_tab = torch.empty(path.table.shape, dtype=torch.int32).pin_memory()

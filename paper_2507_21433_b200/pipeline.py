@@ -52,10 +52,21 @@ class MemSharePath:
         self.final = torch.as_tensor(np.ascontiguousarray(final, np.uint8), device=self.dev)
         table = np.ascontiguousarray(table, np.int32)
         self.table_stride = int(table.shape[1])
-        self.table = _dev_i32(table, self.dev)
-        self.refcount = _dev_i32(refcount, self.dev)
-        self.free_list = _dev_i32(free_list, self.dev)
-        self.free_count = torch.tensor([int(free_count)], dtype=torch.int64, device=self.dev)
+        # the serving state remap() mutates, in ONE buffer (a single copy snapshots / restores it):
+        # [free_count int64][block table][refcounts][free list]
+        refcount = np.ascontiguousarray(refcount, np.int32)
+        free_list = np.ascontiguousarray(free_list, np.int32)
+        nt, nr, nf = table.size, refcount.size, free_list.size
+        host = np.zeros(2 + nt + nr + nf, np.int32)
+        host[:2] = np.asarray([int(free_count)], np.int64).view(np.int32)
+        host[2:2 + nt] = table.ravel()
+        host[2 + nt:2 + nt + nr] = refcount
+        host[2 + nt + nr:] = free_list
+        self.state = torch.as_tensor(host, device=self.dev)
+        self.free_count = self.state[:2].view(torch.int64)
+        self.table = self.state[2:2 + nt].view(table.shape)
+        self.refcount = self.state[2 + nt:2 + nt + nr]
+        self.free_list = self.state[2 + nt + nr:]
         self.num_blocks = int(num_blocks)
         self.k_pool, self.v_pool = k_pool, v_pool
         self.pool = L.KVPool(k_pool.data_ptr() if k_pool is not None else None,

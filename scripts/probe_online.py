@@ -22,7 +22,11 @@ path = MemSharePath(b.tokens, b.seq_tok_off, b.gen_start, b.final, b.delim_ids, 
 path.autosize(w.tau_s)
 torch.cuda.synchronize()
 mode = sys.argv[1] if len(sys.argv) > 1 else "time"
-phases = {"segment": path.segment, "candidates_last": lambda: path.candidates(w.tau_s, cur_mode=L.CUR_LAST),
+offline = "offline" in sys.argv
+cm = L.CUR_ALL if offline else L.CUR_LAST
+pristine = path.state.clone()
+phases = {"restore": lambda: path.state.copy_(pristine, non_blocking=True), "segment": path.segment,
+          "candidates": lambda: path.candidates(w.tau_s, cur_mode=cm),
           "distance": lambda: path.distance_call(w.tau_b), "remap": path.remap}
 if mode == "ncu":
     for _ in range(3):
