@@ -63,6 +63,12 @@ def lib():
         L.oracle_remap.restype = ctypes.c_int
         L.oracle_block_cosine.argtypes = [P, P, I64, I64, I32, I32, I32, I32, P, P, I64, P]
         L.oracle_block_cosine.restype = None
+        L.oracle_kv_append.argtypes = [P, P, I64, I64, I32, I32, I32, I32, P, I32, I32, P, P, P, I32, P, P, P, P]
+        L.oracle_kv_append.restype = ctypes.c_int
+        L.oracle_paged_attention.argtypes = [P, P, I64, I64, I32, I32, I32, I32, P, I32, P, I32, P, I32, F64, P]
+        L.oracle_paged_attention.restype = ctypes.c_int
+        L.oracle_admit.argtypes = [P, I32, I32, I32, I64, P]
+        L.oracle_admit.restype = I32
         L.oracle_similarity_ratio.argtypes = [P, P, I64, I32, P]
         L.oracle_similarity_ratio.restype = None
         L.oracle_all_pairs.argtypes = [P, I32, P, P, P, I32, I32] + [P] * 6 + [I64, P, I64, P]
@@ -243,3 +249,41 @@ def block_cosine(k, v, layer_stride, block_stride, num_layers, h_local, head_dim
     lib().oracle_block_cosine(_p(k), _p(v), layer_stride, block_stride, num_layers, h_local, head_dim, block_size,
                               _p(tp), _p(sp), tp.size, _p(D))
     return D
+
+
+# ---------------------------------------------------------------- f1 decode-loop integration
+def kv_append(k, v, layer_stride, block_stride, num_layers, h, head_dim, block_size, table, seq_len, active,
+              refcount, free_list, free_count, new_k, new_v):
+    """Paged KV append (reading R35) on copies. Returns (status, k, v, table, seq_len, refcount,
+    free_list, free_count)."""
+    k, v = _c(k, np.uint16).copy(), _c(v, np.uint16).copy()
+    tab, sl = _c(table, np.int32).copy(), _c(seq_len, np.int32).copy()
+    rc, fl = _c(refcount, np.int32).copy(), _c(free_list, np.int32).copy()
+    fc = np.asarray([free_count], np.int64)
+    act = None if active is None else _c(active, np.uint8)
+    nk, nv = _c(new_k, np.uint16), _c(new_v, np.uint16)
+    st = lib().oracle_kv_append(_p(k), _p(v), layer_stride, block_stride, num_layers, h, head_dim, block_size,
+                                _p(tab), tab.shape[1], tab.shape[0], _p(sl), None if act is None else _p(act),
+                                _p(rc), rc.size, _p(fl), _p(fc), _p(nk), _p(nv))
+    return st, k, v, tab, sl, rc, fl, int(fc[0])
+
+
+def paged_attention(k, v, layer_stride, block_stride, layer, h, head_dim, block_size, q, num_q_heads, table,
+                    seq_len, scale):
+    """fp64 decode attention through the block table (reading R36): out [S][hq][d_h]."""
+    k, v, q = _c(k, np.uint16), _c(v, np.uint16), _c(q, np.uint16)
+    tab, sl = _c(table, np.int32), _c(seq_len, np.int32)
+    out = np.zeros((sl.size, num_q_heads, head_dim), np.float64)
+    st = lib().oracle_paged_attention(_p(k), _p(v), layer_stride, block_stride, layer, h, head_dim, block_size,
+                                      _p(q), num_q_heads, _p(tab), tab.shape[1], _p(sl), sl.size, scale, _p(out))
+    if st != 0:
+        raise ValueError("paged_attention: invalid arguments")
+    return out
+
+
+def admit(prompt_len, reserve, block_size, free_blocks):
+    """FCFS block-budget admission (reading R37): (admitted, blocks_used)."""
+    pl = _c(prompt_len, np.int32)
+    used = np.zeros(1, np.int64)
+    n = lib().oracle_admit(_p(pl), pl.size, reserve, block_size, free_blocks, _p(used))
+    return int(n), int(used[0])

@@ -502,3 +502,131 @@ void oracle_block_cosine(const uint16_t* k, const uint16_t* v, int64_t layer_str
     D[p] = 1.0 - acc / num_layers;
   }
 }
+
+/* ------------------------------------------------------------------------------------
+ * f1. Decode-loop integration (shared blocks are read "through the block
+ * table" by paged attention; :322 vLLM). Readings R35-R37.
+ * ------------------------------------------------------------------------------------ */
+
+/* Paged KV append of one decode token per active sequence (reading R35). Sequences are visited
+ * in index order; a sequence whose length is a multiple of d takes a fresh block from the END of
+ * the free list (LIFO: the last block freed by remap is reused first). The call is all-or-nothing:
+ * it returns OR_CAPACITY (nothing changed) if the fresh blocks needed exceed free_count or a
+ * position exceeds the table row, and OR_CORRUPTION if a tail block being appended to is not
+ * private (refcount != 1) or a popped block is not free (refcount != 0).
+ * new_k / new_v: bf16 [num_layers][num_seqs][h][d_h]. */
+int oracle_kv_append(uint16_t* k, uint16_t* v, int64_t layer_stride, int64_t block_stride, int32_t num_layers,
+                     int32_t h, int32_t head_dim, int32_t block_size, int32_t* block_table, int32_t table_stride,
+                     int32_t num_seqs, int32_t* seq_len, const uint8_t* active, int32_t* refcount, int32_t num_blocks,
+                     int32_t* free_list, int64_t* free_count, const uint16_t* new_k, const uint16_t* new_v) {
+  int64_t need = 0;
+  for (int32_t s = 0; s < num_seqs; ++s) {
+    if (active && !active[s]) continue;
+    const int32_t pos = seq_len[s];
+    if (pos < 0) return OR_INVALID;
+    const int32_t lb = pos / block_size, off = pos % block_size;
+    if (lb >= table_stride) return OR_CAPACITY;
+    if (off == 0) {
+      ++need;
+    } else {
+      const int32_t b = block_table[(int64_t)s * table_stride + lb];
+      if (b < 0 || b >= num_blocks || refcount[b] != 1) return OR_CORRUPTION;
+    }
+  }
+  if (need > *free_count) return OR_CAPACITY;
+  for (int64_t r = 0; r < need; ++r) {
+    const int32_t b = free_list[*free_count - 1 - r];
+    if (b < 0 || b >= num_blocks || refcount[b] != 0) return OR_CORRUPTION;
+  }
+  const int64_t row = (int64_t)h * head_dim;
+  for (int32_t s = 0; s < num_seqs; ++s) {
+    if (active && !active[s]) continue;
+    const int32_t pos = seq_len[s];
+    const int32_t lb = pos / block_size, off = pos % block_size;
+    int32_t b;
+    if (off == 0) {
+      *free_count -= 1;
+      b = free_list[*free_count];
+      refcount[b] = 1;
+      block_table[(int64_t)s * table_stride + lb] = b;
+    } else {
+      b = block_table[(int64_t)s * table_stride + lb];
+    }
+    for (int32_t l = 0; l < num_layers; ++l) {
+      const int64_t dst = (int64_t)l * layer_stride + (int64_t)b * block_stride + (int64_t)off * row;
+      const int64_t src = ((int64_t)l * num_seqs + s) * row;
+      for (int64_t e = 0; e < row; ++e) {
+        k[dst + e] = new_k[src + e];
+        v[dst + e] = new_v[src + e];
+      }
+    }
+    seq_len[s] = pos + 1;
+  }
+  return OR_OK;
+}
+
+/* Decode attention of one layer through the block table (reading R36): for sequence s and query
+ * head qh (KV head g = qh / (hq / h), GQA),
+ *   score_j = scale * <q[s][qh], K_l[table[s][j / d]][j % d][g]>,  j < seq_len[s]
+ *   out[s][qh] = sum_j softmax(score)_j * V_l[table[s][j / d]][j % d][g]
+ * in fp64 (q is bf16, as the kernel reads it). seq_len[s] == 0 gives a zero output. */
+int oracle_paged_attention(const uint16_t* k, const uint16_t* v, int64_t layer_stride, int64_t block_stride,
+                           int32_t layer, int32_t h, int32_t head_dim, int32_t block_size, const uint16_t* q,
+                           int32_t num_q_heads, const int32_t* block_table, int32_t table_stride,
+                           const int32_t* seq_len, int32_t num_seqs, double scale, double* out) {
+  if (h < 1 || num_q_heads < h || num_q_heads % h != 0) return OR_INVALID;
+  const int32_t G = num_q_heads / h;
+  for (int32_t s = 0; s < num_seqs; ++s) {
+    const int32_t n = seq_len[s];
+    double* sc = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int32_t qh = 0; qh < num_q_heads; ++qh) {
+      const int32_t g = qh / G;
+      const uint16_t* qv = q + ((int64_t)s * num_q_heads + qh) * head_dim;
+      double* o = out + ((int64_t)s * num_q_heads + qh) * head_dim;
+      for (int32_t x = 0; x < head_dim; ++x) o[x] = 0.0;
+      if (n == 0) continue;
+      double mx = -INFINITY;
+      for (int32_t j = 0; j < n; ++j) {
+        const int32_t b = block_table[(int64_t)s * table_stride + j / block_size];
+        const uint16_t* kr = k + (int64_t)layer * layer_stride + (int64_t)b * block_stride +
+                             ((int64_t)(j % block_size) * h + g) * head_dim;
+        double dot = 0.0;
+        for (int32_t x = 0; x < head_dim; ++x) dot += bf16_to_double(qv[x]) * bf16_to_double(kr[x]);
+        sc[j] = scale * dot;
+        if (sc[j] > mx) mx = sc[j];
+      }
+      double z = 0.0;
+      for (int32_t j = 0; j < n; ++j) {
+        sc[j] = exp(sc[j] - mx);
+        z += sc[j];
+      }
+      for (int32_t j = 0; j < n; ++j) {
+        const int32_t b = block_table[(int64_t)s * table_stride + j / block_size];
+        const uint16_t* vr = v + (int64_t)layer * layer_stride + (int64_t)b * block_stride +
+                             ((int64_t)(j % block_size) * h + g) * head_dim;
+        const double p = sc[j] / z;
+        for (int32_t x = 0; x < head_dim; ++x) o[x] += p * bf16_to_double(vr[x]);
+      }
+    }
+    free(sc);
+  }
+  return OR_OK;
+}
+
+/* Block-budget admission (reading R37; the mechanism behind PAPER.md Fig. 6: blocks freed by
+ * sharing admit more concurrent sequences). Waiting requests are taken first-come-first-served;
+ * request i needs ceil((prompt_len[i] + reserve) / d) blocks; it is admitted while the need fits
+ * in the free blocks left, and admission stops at the first request that does not fit (no
+ * skipping ahead). Returns the number admitted; blocks_used receives their total need. */
+int32_t oracle_admit(const int32_t* prompt_len, int32_t num_waiting, int32_t reserve, int32_t block_size,
+                     int64_t free_blocks, int64_t* blocks_used) {
+  int64_t used = 0;
+  int32_t i = 0;
+  for (; i < num_waiting; ++i) {
+    const int64_t need = ((int64_t)prompt_len[i] + reserve + block_size - 1) / block_size;
+    if (used + need > free_blocks) break;
+    used += need;
+  }
+  *blocks_used = used;
+  return i;
+}
