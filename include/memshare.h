@@ -269,6 +269,66 @@ const char* memshare_status_string(memshare_status status);
 /* MEMSHARE_ABI_VERSION of the loaded library. */
 int32_t memshare_abi_version(void);
 
+/* ---------------------------------------------------------------------------------------- f1
+ * Decode-loop integration: the steps on either side of the MemShare path. Shared blocks are
+ * read "through the block table" by paged attention, with no copy.
+ *
+ * memshare_kv_append -- one decode token per active sequence into the paged pool (reading R35).
+ *   k_pool/v_pool   bf16 device pools, layout K[l][block][tau][head][x] (written)
+ *   layer_stride, block_stride, num_blocks   as in memshare_kv_pool (elements; multiples of 8)
+ *   dims_host       num_layers, num_kv_heads_local (heads stored in the pool), head_dim, block_size
+ *   block_table     int32 [num_seqs][table_stride] (device, updated)
+ *   seq_len         int32 [num_seqs] tokens already stored per sequence (device, +1 per active)
+ *   active          uint8 [num_seqs] or NULL (= all active)
+ *   refcount        int32 [num_blocks]; free_list int32 [..]; free_count int64 [1] (device, updated)
+ *   new_k/new_v     bf16 [num_layers][num_seqs][num_kv_heads_local][head_dim] (device, 16-byte aligned)
+ * Sequence s writes its row at position seq_len[s]; when seq_len[s] % block_size == 0 it first
+ * takes a fresh block from the END of the free list (LIFO, in sequence order), sets its refcount
+ * to 1 and enters it in the table. All-or-nothing: on a device-detected error nothing changes and
+ * device_status receives CAPACITY (not enough free blocks, or the table row is full),
+ * CORRUPTION (the tail block is shared, refcount != 1, or a popped block is not free) or
+ * INVALID_ARGUMENT (negative seq_len). Host errors: INVALID_ARGUMENT. */
+memshare_status memshare_kv_append(void* k_pool, void* v_pool, int64_t layer_stride, int64_t block_stride,
+                                   int32_t num_blocks, const memshare_dims* dims_host, int32_t* block_table,
+                                   int32_t table_stride, int32_t num_seqs, int32_t* seq_len, const uint8_t* active,
+                                   int32_t* refcount, int32_t* free_list, int64_t* free_count, const void* new_k,
+                                   const void* new_v, void* workspace, size_t workspace_bytes, int32_t* device_status,
+                                   void* stream);
+size_t memshare_kv_append_workspace_size(int32_t num_seqs);
+
+/* memshare_paged_attention_decode -- one layer of GQA decode attention through the block table
+ * (reading R36): for sequence s and query head qh (KV head g = qh / (num_q_heads / h_local)),
+ *   out[s][qh] = sum_{j < seq_len[s]} softmax_j(scale * <q[s][qh], K_l[table[s][j/d]][j%d][g]>)
+ *                * V_l[table[s][j/d]][j%d][g]
+ *   pool_host/dims_host  the KV pool (block_size must be 16, head_dim 64 or 128)
+ *   layer           which layer l
+ *   q               bf16 [num_seqs][num_q_heads][head_dim] (device); num_q_heads = G * h_local,
+ *                   1 <= G <= 8
+ *   seq_len         int32 [num_seqs] (device); 0 gives a zero output
+ *   max_seq_len     host upper bound of seq_len (sizes the split-KV grid and the workspace);
+ *                   table_stride >= ceil(max_seq_len / 16)
+ *   out             fp32 [num_seqs][num_q_heads][head_dim] (device)
+ * Implementation: split-KV over 256-token chunks (one CTA per chunk x KV head x sequence, fp32
+ * online softmax), then one warp per (sequence, query head) combines the chunks. A table entry
+ * outside [0, num_blocks) sets CORRUPTION. Host errors: INVALID_ARGUMENT. */
+memshare_status memshare_paged_attention_decode(const memshare_kv_pool* pool_host, const memshare_dims* dims_host,
+                                                int32_t layer, const void* q, int32_t num_q_heads,
+                                                const int32_t* block_table, int32_t table_stride,
+                                                const int32_t* seq_len, int32_t num_seqs, int32_t max_seq_len,
+                                                float scale, float* out, void* workspace, size_t workspace_bytes,
+                                                int32_t* device_status, void* stream);
+size_t memshare_paged_attention_workspace_size(const memshare_dims* dims_host, int32_t num_seqs, int32_t num_q_heads,
+                                               int32_t max_seq_len);
+
+/* memshare_admit -- HOST function, block-budget admission (reading R37; the mechanism behind
+ * PAPER.md Fig. 6: blocks freed by sharing admit more concurrent sequences). Waiting request i
+ * (in queue order) needs ceil((prompt_len_host[i] + reserve) / block_size) blocks; requests are
+ * admitted first-come-first-served while their need fits in free_blocks and admission stops at
+ * the first that does not fit. Returns the number admitted (a prefix of the queue) and writes
+ * their total need to *blocks_used_host (if not NULL); -1 for invalid arguments. */
+int32_t memshare_admit(const int32_t* prompt_len_host, int32_t num_waiting, int32_t reserve, int32_t block_size,
+                       int64_t free_blocks, int64_t* blocks_used_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,16 @@ def _load():
     L.memshare_all_pairs.restype = I32
     L.memshare_all_pairs_workspace_size.argtypes = [I32]
     L.memshare_all_pairs_workspace_size.restype = U64
+    L.memshare_kv_append.argtypes = [P, P, I64, I64, I32, P, P, I32, I32, P, P, P, P, P, P, P, P, U64, P, P]
+    L.memshare_kv_append.restype = I32
+    L.memshare_kv_append_workspace_size.argtypes = [I32]
+    L.memshare_kv_append_workspace_size.restype = U64
+    L.memshare_paged_attention_decode.argtypes = [P, P, I32, P, I32, P, I32, P, I32, I32, F32, P, P, U64, P, P]
+    L.memshare_paged_attention_decode.restype = I32
+    L.memshare_paged_attention_workspace_size.argtypes = [P, I32, I32, I32]
+    L.memshare_paged_attention_workspace_size.restype = U64
+    L.memshare_admit.argtypes = [P, I32, I32, I32, I64, P]
+    L.memshare_admit.restype = I32
     L.memshare_status_string.argtypes = [I32]
     L.memshare_status_string.restype = ctypes.c_char_p
     L.memshare_abi_version.argtypes = []
@@ -192,3 +202,44 @@ def all_pairs(seq_tok_off, num_seqs, blk_begin, blk_end, block_table, table_stri
                                   _ptr(target_off), target_cap, _ptr(num_targets), _ptr(workspace),
                                   0 if workspace is None else workspace.numel() * workspace.element_size(),
                                   _ptr(device_status), _stream(stream))
+
+
+# -------------------------------------------------------------------------------------- f1
+def kv_append_workspace_size(num_seqs: int) -> int:
+    return lib.memshare_kv_append_workspace_size(num_seqs)
+
+
+def kv_append(k_pool, v_pool, layer_stride, block_stride, num_blocks, dims: Dims, block_table, table_stride,
+              num_seqs, seq_len, active, refcount, free_list, free_count, new_k, new_v, workspace, device_status,
+              stream=None) -> int:
+    return lib.memshare_kv_append(_ptr(k_pool), _ptr(v_pool), layer_stride, block_stride, num_blocks,
+                                  ctypes.byref(dims), _ptr(block_table), table_stride, num_seqs, _ptr(seq_len),
+                                  _ptr(active), _ptr(refcount), _ptr(free_list), _ptr(free_count), _ptr(new_k),
+                                  _ptr(new_v), _ptr(workspace),
+                                  0 if workspace is None else workspace.numel() * workspace.element_size(),
+                                  _ptr(device_status), _stream(stream))
+
+
+def paged_attention_workspace_size(dims: Dims, num_seqs: int, num_q_heads: int, max_seq_len: int) -> int:
+    return lib.memshare_paged_attention_workspace_size(ctypes.byref(dims), num_seqs, num_q_heads, max_seq_len)
+
+
+def paged_attention_decode(pool: KVPool, dims: Dims, layer, q, num_q_heads, block_table, table_stride, seq_len,
+                           num_seqs, max_seq_len, scale, out, workspace, device_status, stream=None) -> int:
+    return lib.memshare_paged_attention_decode(ctypes.byref(pool), ctypes.byref(dims), layer, _ptr(q), num_q_heads,
+                                               _ptr(block_table), table_stride, _ptr(seq_len), num_seqs, max_seq_len,
+                                               float(scale), _ptr(out), _ptr(workspace),
+                                               0 if workspace is None else workspace.numel() * workspace.element_size(),
+                                               _ptr(device_status), _stream(stream))
+
+
+def admit(prompt_len, reserve: int, block_size: int, free_blocks: int):
+    """Host FCFS block-budget admission (native): (admitted, blocks_used)."""
+    import numpy as _np
+    pl = _np.ascontiguousarray(prompt_len, _np.int32)
+    used = ctypes.c_int64(0)
+    n = lib.memshare_admit(pl.ctypes.data if pl.size else None, pl.size, reserve, block_size, free_blocks,
+                           ctypes.byref(used))
+    if n < 0:
+        raise MemShareError("admit: invalid arguments")
+    return int(n), int(used.value)

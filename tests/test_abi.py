@@ -72,3 +72,32 @@ def test_invalid_arguments_rejected_before_any_launch(lib):
     assert L.memshare_block_distance(nul, ctypes.byref(dims), nul, nul, nul, nul, 0, 0, 0, 0, nul, 0.1, nul, nul,
                                      nul, nul, 0, nul, nul) == 1
     assert L.memshare_remap(nul, 0, 0, nul, 0, nul, nul, nul, nul, 0, 16, nul, nul, nul, 0, nul, nul) == 1
+
+
+def test_f1_host_checks_and_admission(lib):
+    L = lib.lib
+    nul = None
+    dims = lib.Dims(64, 8, 8, 128, 16)
+    # kv_append: null workspace / bad dims -> INVALID_ARGUMENT
+    assert L.memshare_kv_append(nul, nul, 0, 0, 0, ctypes.byref(dims), nul, 0, 1, nul, nul, nul, nul, nul, nul, nul,
+                                nul, 0, nul, nul) == 1
+    # attention: block_size must be 16, head_dim 64/128, G <= 8
+    bad = lib.Dims(64, 8, 8, 96, 16)
+    pool = lib.KVPool(None, None, 0, 0, 0, 0)
+    ws = (ctypes.c_char * 64)()
+    st = (ctypes.c_int32 * 1)()
+    assert L.memshare_paged_attention_decode(ctypes.byref(pool), ctypes.byref(bad), 0, nul, 40, nul, 1, nul, 1, 16,
+                                             0.1, nul, ws, 64, st, nul) == 1
+    assert L.memshare_paged_attention_decode(ctypes.byref(pool), ctypes.byref(dims), 0, nul, 72, nul, 1, nul, 1, 16,
+                                             0.1, nul, ws, 64, st, nul) == 1
+    assert lib.paged_attention_workspace_size(dims, 4, 40, 12406) >= 4 * 40 * 49 * 130 * 4
+    assert lib.kv_append_workspace_size(8) > 0
+    # the native admission scheduler against the oracle's definition on random queues
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        pl = rng.integers(0, 400, rng.integers(0, 12))
+        r, bsz, fb = int(rng.integers(0, 64)), int(rng.choice([1, 16, 32])), int(rng.integers(0, 80))
+        assert lib.admit(pl, r, bsz, fb) == oracle.admit(pl, r, bsz, fb)
+    assert L.memshare_admit(nul, 2, 0, 16, 10, nul) == -1
