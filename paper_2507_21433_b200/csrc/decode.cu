@@ -135,7 +135,6 @@ constexpr int kBlk = 16;               // tokens per KV block (the lane mapping 
 constexpr int kChunkBlocks = 16;       // blocks per CTA work item (256 tokens)
 constexpr int kAttWarps = 4;
 constexpr int kAttNT = kAttWarps * 32;
-constexpr int kBlocksPerWarp = kChunkBlocks / kAttWarps;
 constexpr int kMaxG = 8;               // query heads per KV head
 
 struct AttArgs {
@@ -156,146 +155,193 @@ struct AttArgs {
   int32_t* status;
 };
 
-__device__ __forceinline__ float2 bf2f(uint32_t x) {
-  return make_float2(__uint_as_float(x << 16), __uint_as_float(x & 0xFFFF0000u));
-}
+// ---- tensor-core building blocks (mma.sync m16n8k16 bf16 -> fp32, ldmatrix, cp.async) ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// One CTA per (chunk, kv head g, sequence s); warp w handles kBlocksPerWarp consecutive blocks.
-// Lanes map to (token t = lane / 2, half) for the q.k scores (d_h / 2 dims each, q in smem) and to
-// d_h / 32 contiguous dims for the p.V accumulation (p in smem).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int n = valid ? 16 : 0;                     // src-size 0: zero-fill (rows past the sequence end)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+// D = A(16x16 bf16, row) * B(16x8 bf16, col) + D (fp32)
+__device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float bf16_lo(uint32_t x) { return __uint_as_float(x << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
+
+// One CTA per (256-token chunk, KV head g, sequence s); warp w handles blocks w, w+4, w+8, w+12
+// of the chunk. Per 16-token block and KV head, the K and V rows (16 x d_h bf16 each) are staged
+// in XOR-swizzled smem by cp.async (double-buffered per warp) and both contractions run on the
+// tensor cores (mma.sync m16n8k16, fp32 accumulate):
+//   S   = Q K^T   A = Q (the G <= 8 query heads of g, zero-padded to 16 rows, in registers),
+//                 B = K rows via ldmatrix; C rows = query heads, cols = tokens
+//   O^T += V^T P^T  A = V^T via ldmatrix.trans, B = P taken straight from S's C fragments,
+//                 split into bf16 hi + lo parts (two MMAs: ~16-bit P keeps the result within
+//                 fp32-accumulation error of the fp64 oracle); C rows = dims, cols = query heads
+// with an fp32 online softmax in between (row statistics per query head).
 template <int DH>
 __global__ void __launch_bounds__(kAttNT) attn_split_kernel(AttArgs a) {
-  constexpr int HALF = DH / 2;
-  constexpr int QROW = DH + 4;                       // padded: the two halves sit in different banks
-  constexpr int VPL = DH / 32;                        // V dims per lane
-  __shared__ __align__(16) float sq[kMaxG][QROW];
-  __shared__ float sp[kAttWarps][kMaxG][kBlk];
+  constexpr int KS = DH / 16;                 // k-steps of Q K^T
+  constexpr int MT = DH / 16;                 // m-tiles (16 dims) of O^T
+  constexpr int CH = DH / 8;                  // 16-byte chunks per row
+  constexpr int ROWB = DH * 2;                // bytes per K/V row in smem
+  constexpr int TILE = kBlk * ROWB;           // one K or V tile
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* s_kv = smem;                                        // [warp][stage][K|V][TILE]
+  float* s_acc = reinterpret_cast<float*>(smem);                     // [warp][kMaxG][DH], after the loop
   __shared__ float s_m[kAttWarps][kMaxG], s_l[kAttWarps][kMaxG];
-  __shared__ __align__(16) float s_acc[kAttWarps][kMaxG][DH];
   const int chunk = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = a.G;
   const int32_t len = a.seq_len[s];
   const int32_t tok0 = chunk * kChunkBlocks * kBlk;
   if (tok0 >= len) return;
-  // q of this KV head's query heads -> fp32 smem
-  for (int i = threadIdx.x; i < G * DH; i += kAttNT) {
-    const int qi = i / DH, x = i % DH;
-    const uint16_t b = a.q[((int64_t)s * a.h * G + (int64_t)g * G + qi) * DH + x];
-    sq[qi][x + (x >= HALF ? 4 : 0)] = __uint_as_float((uint32_t)b << 16);
-  }
-  __syncthreads();
-  float m[kMaxG], l[kMaxG], acc[kMaxG][VPL];
+  const int r0 = lane >> 2, c2 = 2 * (lane & 3);
+  // Q as A fragments (rows = query heads of g; rows >= G and rows 8..15 are zero)
+  uint32_t qa0[KS], qa2[KS];
+  {
+    const uint16_t* qb = a.q + ((int64_t)s * a.h * G + (int64_t)g * G) * DH;
+    const bool v0 = r0 < G;
 #pragma unroll
-  for (int i = 0; i < kMaxG; ++i) {
-    m[i] = -INFINITY;
-    l[i] = 0.f;
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) acc[i][j] = 0.f;
+    for (int kk = 0; kk < KS; ++kk) {
+      const int c = kk * 16 + c2;
+      qa0[kk] = v0 ? *reinterpret_cast<const uint32_t*>(qb + r0 * DH + c) : 0u;
+      qa2[kk] = v0 ? *reinterpret_cast<const uint32_t*>(qb + r0 * DH + c + 8) : 0u;
+    }
   }
-  const int t = lane >> 1, half = lane & 1;
-  const float* qh_base = &sq[0][half * (HALF + 4)];
+  float o[MT][4];                              // O^T: rows dims mt*16 + r0 (+8), cols q = c2 (+1)
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+  float m_r = -INFINITY, l_r = 0.f;           // softmax statistics of query head r0
   const int32_t* trow = a.table + (int64_t)s * a.stride;
-  const uint16_t* kl = a.k + (int64_t)a.layer * a.layer_stride;
-  const uint16_t* vl = a.v + (int64_t)a.layer * a.layer_stride;
+  const uint16_t* kl = a.k + (int64_t)a.layer * a.layer_stride + g * DH;
+  const uint16_t* vl = a.v + (int64_t)a.layer * a.layer_stride + g * DH;
   const int64_t row = (int64_t)a.h * DH;
-  for (int bi = 0; bi < kBlocksPerWarp; ++bi) {
-    const int32_t lb = chunk * kChunkBlocks + w * kBlocksPerWarp + bi;
-    const int32_t j0 = lb * kBlk;
-    if (j0 >= len) break;
-    const int ntok = min(kBlk, len - j0);
+  const int32_t nblk_seq = (len + kBlk - 1) / kBlk;
+  bool bad = false;
+  auto tile = [&](int st, int kv) { return smem_addr(s_kv + (((w * 2 + st) * 2 + kv) * TILE)); };
+  auto issue = [&](int bi, int st) -> bool {
+    const int32_t lb = chunk * kChunkBlocks + w + bi * kAttWarps;
+    if (bi * kAttWarps >= kChunkBlocks || lb >= nblk_seq) return false;
     const int32_t blk = trow[lb];
-    if (blk < 0 || blk >= a.num_blocks) {
-      if (lane == 0) set_status(a.status, MEMSHARE_ERR_CORRUPTION);
-      break;
-    }
-    const uint16_t* kb = kl + (int64_t)blk * a.block_stride + g * DH;
-    const uint16_t* vb = vl + (int64_t)blk * a.block_stride + g * DH;
-    // issue the V loads of this block first (independent of the scores)
-    uint2 vr[kBlk];
+    if (blk < 0 || blk >= a.num_blocks) { bad = true; return false; }
+    const int ntok = min(kBlk, len - lb * kBlk);
+    const uint16_t* kb = kl + (int64_t)blk * a.block_stride;
+    const uint16_t* vb = vl + (int64_t)blk * a.block_stride;
+    const uint32_t sk = tile(st, 0), sv = tile(st, 1);
 #pragma unroll
-    for (int tt = 0; tt < kBlk; ++tt) {
-      vr[tt] = make_uint2(0u, 0u);
-      if (tt < ntok) {
-        if constexpr (VPL == 4) vr[tt] = __ldg(reinterpret_cast<const uint2*>(vb + tt * row) + lane);
-        else vr[tt].x = __ldg(reinterpret_cast<const uint32_t*>(vb + tt * row) + lane);
+    for (int i = 0; i < (kBlk * CH) / 32; ++i) {
+      const int id = lane + 32 * i, t = id / CH, c = id % CH;
+      const uint32_t off = t * ROWB + ((c ^ (t & 7)) << 4);
+      cp_async16(sk + off, kb + t * row + c * 8, t < ntok);
+      cp_async16(sv + off, vb + t * row + c * 8, t < ntok);
+    }
+    return true;
+  };
+  const uint32_t zero = 0u;
+  bool have = issue(0, 0);
+  cp_async_commit();
+  for (int bi = 0; have; ++bi) {
+    const int st = bi & 1;
+    const bool next = issue(bi + 1, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int32_t lb = chunk * kChunkBlocks + w + bi * kAttWarps;
+    const int ntok = min(kBlk, len - lb * kBlk);
+    const uint32_t sk = tile(st, 0), sv = tile(st, 1);
+    // S = Q K^T, two n-tiles of 8 tokens
+    float sc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < KS; kk += 2) {
+        const int t = nt * 8 + (lane & 7), c = kk * 2 + (lane >> 3);     // 4 matrices: 2 k-steps
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(sk + t * ROWB + ((c ^ (t & 7)) << 4), b0, b1, b2, b3);
+        mma_bf16(sc[nt], qa0[kk], zero, qa2[kk], zero, b0, b1);
+        mma_bf16(sc[nt], qa0[kk + 1], zero, qa2[kk + 1], zero, b2, b3);
       }
     }
-    // K row half of token t
-    uint4 kr[HALF / 8];
-    const uint4* kp = reinterpret_cast<const uint4*>(kb + t * row + half * HALF);
+    // online softmax of query head r0 over this block's tokens
+    float mx = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < HALF / 8; ++c) kr[c] = t < ntok ? __ldg(kp + c) : make_uint4(0u, 0u, 0u, 0u);
-    float sc[kMaxG];
+    for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
-    for (int qi = 0; qi < kMaxG; ++qi) {
-      if (qi < G) {
-        const float* qv = qh_base + qi * QROW;
-        float2 d = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < HALF / 8; ++c) {
-          const float4 q0 = *reinterpret_cast<const float4*>(qv + c * 8);
-          const float4 q1 = *reinterpret_cast<const float4*>(qv + c * 8 + 4);
-          d = __ffma2_rn(make_float2(q0.x, q0.y), bf2f(kr[c].x), d);
-          d = __ffma2_rn(make_float2(q0.z, q0.w), bf2f(kr[c].y), d);
-          d = __ffma2_rn(make_float2(q1.x, q1.y), bf2f(kr[c].z), d);
-          d = __ffma2_rn(make_float2(q1.z, q1.w), bf2f(kr[c].w), d);
-        }
-        float x = d.x + d.y;
-        x += __shfl_xor_sync(0xffffffffu, x, 1);
-        sc[qi] = t < ntok ? x * a.scale : -INFINITY;
+      for (int j = 0; j < 2; ++j) {
+        const int t = nt * 8 + c2 + j;
+        sc[nt][j] = t < ntok ? sc[nt][j] * a.scale : -INFINITY;
+        mx = fmaxf(mx, sc[nt][j]);
       }
     }
-    // online softmax over this block's tokens
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m_r, mx);
+    const float corr = __expf(m_r - mn);
+    m_r = mn;
+    float p[2][2], ps = 0.f;
 #pragma unroll
-    for (int qi = 0; qi < kMaxG; ++qi) {
-      if (qi < G) {
-        float bm = sc[qi];
+    for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-        for (int o = 2; o < 32; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-        const float mn = fmaxf(m[qi], bm);
-        const float corr = __expf(m[qi] - mn);
-        const float p = __expf(sc[qi] - mn);
-        float ps = half == 0 ? p : 0.f;
+      for (int j = 0; j < 2; ++j) { p[nt][j] = __expf(sc[nt][j] - mn); ps += p[nt][j]; }
+    l_r = l_r * corr + ps;
+    // O^T columns are query heads c2, c2 + 1: their rescale factors live in lanes 4*c2, 4*(c2+1)
+    const float cq0 = __shfl_sync(0xffffffffu, corr, 4 * c2), cq1 = __shfl_sync(0xffffffffu, corr, 4 * (c2 + 1));
 #pragma unroll
-        for (int o = 2; o < 32; o <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-        l[qi] = l[qi] * corr + ps;
-        m[qi] = mn;
+    for (int mt = 0; mt < MT; ++mt) { o[mt][0] *= cq0; o[mt][1] *= cq1; o[mt][2] *= cq0; o[mt][3] *= cq1; }
+    // P^T as B fragments: (k = token, n = query head) = S C fragments of the two n-tiles
+    const uint32_t bh0 = pack_bf16(p[0][0], p[0][1]), bh1 = pack_bf16(p[1][0], p[1][1]);
+    const uint32_t bl0 = pack_bf16(p[0][0] - bf16_lo(bh0), p[0][1] - bf16_hi(bh0));
+    const uint32_t bl1 = pack_bf16(p[1][0] - bf16_lo(bh1), p[1][1] - bf16_hi(bh1));
+    // O^T += V^T P^T; V^T fragments via ldmatrix.trans of the [token][dim] rows
 #pragma unroll
-        for (int j = 0; j < VPL; ++j) acc[qi][j] *= corr;
-        if (half == 0) sp[w][qi][t] = p;
-      }
+    for (int mt = 0; mt < MT; ++mt) {
+      const int mi = lane >> 3, t = (mi >> 1) * 8 + (lane & 7), c = mt * 2 + (mi & 1);
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4_t(sv + t * ROWB + ((c ^ (t & 7)) << 4), a0, a1, a2, a3);
+      mma_bf16(o[mt], a0, a1, a2, a3, bh0, bh1);
+      mma_bf16(o[mt], a0, a1, a2, a3, bl0, bl1);
     }
     __syncwarp();
-#pragma unroll
-    for (int tt = 0; tt < kBlk; ++tt) {
-      if (tt < ntok) {
-        const float2 v01 = bf2f(vr[tt].x);
-        float2 v23 = make_float2(0.f, 0.f);
-        if (VPL == 4) v23 = bf2f(vr[tt].y);
-#pragma unroll
-        for (int qi = 0; qi < kMaxG; ++qi) {
-          if (qi < G) {
-            const float p = sp[w][qi][tt];
-            acc[qi][0] = fmaf(p, v01.x, acc[qi][0]);
-            acc[qi][1] = fmaf(p, v01.y, acc[qi][1]);
-            if (VPL == 4) {
-              acc[qi][VPL - 2] = fmaf(p, v23.x, acc[qi][VPL - 2]);
-              acc[qi][VPL - 1] = fmaf(p, v23.y, acc[qi][VPL - 1]);
-            }
-          }
-        }
-      }
-    }
-    __syncwarp();
+    have = next;
   }
-  // merge the warps' (m, l, acc) and write this chunk's partial
+  cp_async_wait<0>();
+  if (bad) set_status(a.status, MEMSHARE_ERR_CORRUPTION);
+  l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
+  l_r += __shfl_xor_sync(0xffffffffu, l_r, 2);
+  __syncthreads();                            // the K/V stages become s_acc
+  if ((lane & 3) == 0 && r0 < kMaxG) { s_m[w][r0] = m_r; s_l[w][r0] = l_r; }
 #pragma unroll
-  for (int qi = 0; qi < kMaxG; ++qi) {
-    if (qi < G) {
-      if (lane == 0) { s_m[w][qi] = m[qi]; s_l[w][qi] = l[qi]; }
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-      for (int j = 0; j < VPL; ++j) s_acc[w][qi][lane * VPL + j] = acc[qi][j];
+    for (int j = 0; j < 2; ++j) {
+      const int q = c2 + j;
+      if (q < G) {
+        s_acc[(w * kMaxG + q) * DH + mt * 16 + r0] = o[mt][j];
+        s_acc[(w * kMaxG + q) * DH + mt * 16 + r0 + 8] = o[mt][2 + j];
+      }
     }
   }
   __syncthreads();
@@ -310,11 +356,18 @@ __global__ void __launch_bounds__(kAttNT) attn_split_kernel(AttArgs a) {
     for (int ww = 0; ww < kAttWarps; ++ww) {
       const float f = s_m[ww][qi] == -INFINITY ? 0.f : __expf(s_m[ww][qi] - M);
       L += s_l[ww][qi] * f;
-      A += s_acc[ww][qi][x] * f;
+      A += s_acc[(ww * kMaxG + qi) * DH + x] * f;
     }
     a.pacc[(pbase + qi) * DH + x] = A;
     if (x == 0) { a.pm[pbase + qi] = M; a.pl[pbase + qi] = L; }
   }
+}
+
+template <int DH>
+constexpr size_t attn_smem_bytes() {
+  const size_t kv = (size_t)kAttWarps * 2 * 2 * kBlk * DH * 2;
+  const size_t acc = (size_t)kAttWarps * kMaxG * DH * 4;
+  return kv > acc ? kv : acc;
 }
 
 // One warp per (sequence, query head): combine the chunk partials.
@@ -453,14 +506,22 @@ extern "C" memshare_status memshare_paged_attention_decode(
   a.pacc = w.take<float>(parts * d.head_dim);
   a.status = device_status;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)attn_smem_bytes<128>());
+    cudaFuncSetAttribute(attn_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)attn_smem_bytes<64>());
+    attr_set = true;
+  }
   const dim3 grid(a.max_chunks, d.num_kv_heads_local, num_seqs);
   const int64_t warps = (int64_t)num_seqs * num_q_heads;
   const int cgrid = (int)((warps * 32 + 255) / 256);
   if (d.head_dim == 128) {
-    attn_split_kernel<128><<<grid, kAttNT, 0, st>>>(a);
+    attn_split_kernel<128><<<grid, kAttNT, attn_smem_bytes<128>(), st>>>(a);
     attn_combine_kernel<128><<<cgrid, 256, 0, st>>>(a);
   } else {
-    attn_split_kernel<64><<<grid, kAttNT, 0, st>>>(a);
+    attn_split_kernel<64><<<grid, kAttNT, attn_smem_bytes<64>(), st>>>(a);
     attn_combine_kernel<64><<<cgrid, 256, 0, st>>>(a);
   }
   return launch_status();
