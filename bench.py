@@ -371,6 +371,8 @@ def main():
     d_ms = float(np.mean([a.elapsed_time(b_) for a, b_ in d_events]))
     ck = clocks.stop()
     assert path.read_status() == 0
+    # counters of the last timed (offline) step, read before the online / e2e legs overwrite them
+    step_freed, step_affected = int(path.num_freed.item()), int(path.affected.item())
 
     # max over ranks of the step time; sum of pairs over ranks
     t = torch.tensor([ms_total, float(P)], dtype=torch.float64, device=dev)
@@ -525,7 +527,7 @@ def main():
                      "kv_bytes": kv_bytes, "distinct_blocks": U, "peak_source": peak_src,
                      "frac_of_nominal_8000": achieved / 8000.0},
         "per_step": {"pairs": P, "targets": T, "steps": counts["steps"], "matches": counts["matches"],
-                     "freed_blocks": int(path.num_freed.item()), "affected_tokens": int(path.affected.item())},
+                     "freed_blocks": step_freed, "affected_tokens": step_affected},
         "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
         "clocks": {"sm_mhz": ck["sm_mhz"], "sm_max_mhz": ck["sm_max_mhz"], "reasons": ck["reasons"],
                    "samples": ck["samples"]},

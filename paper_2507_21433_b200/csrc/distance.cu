@@ -51,6 +51,12 @@ namespace {
 #ifndef MS_ANCHOR_FP32
 #define MS_ANCHOR_FP32 1          // 1: anchors cached as fp32 (2x registers, no per-pair unpack)
 #endif
+#ifndef MS_PIPE
+#define MS_PIPE 1                 // 1: software-pipelined single-target Euclidean consumers
+#endif
+#ifndef MS_SUB_UNPACK
+#define MS_SUB_UNPACK 0           // 1: t - s via ALU unpack + FFMA2 instead of FHFMA.BF16
+#endif
 constexpr int kConsumerWarps = MS_CONSUMER_WARPS;
 static_assert(kConsumerWarps % 4 == 0, "partials are read as float4");
 constexpr int kConsumers = kConsumerWarps * 32;
@@ -66,6 +72,12 @@ constexpr int kMetaEnt = 4;                         // pairs evaluated against o
 constexpr int kPlanThreads = 1024;
 
 constexpr int F_STOP = 1;
+constexpr int H_STOP = 1, H_ANCHOR = 2, H_PAIR = 4;
+
+// the single-target consumer's view of a stage (one 16-byte shared load)
+__device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t code) {
+  return make_int4((int32_t)(uint32_t)(uint64_t)out, (int32_t)((uint64_t)out >> 32), bytes, code);
+}
 
 // One work item: <= kAnchors targets of one pair-graph component, with the pair range of each.
 struct ItemRec {
@@ -77,6 +89,7 @@ struct ItemRec {
 
 // One ring stage: which slice it holds and which pairs to evaluate against it.
 struct Meta {
+  int4 hdr;                // consumer header: {out lo, out hi, bytes, code} (code: bit0 stop, bit1 anchor, bit2 pair)
   int32_t pair[kMetaEnt];
   int8_t anc[kMetaEnt];    // anchor slot holding the other operand of pair[e]
   int32_t nent;
@@ -484,6 +497,118 @@ __device__ __forceinline__ float dist2_anchor(const AnchorT (&A)[kAnchors], cons
   return (acc0.x + acc0.y) + (acc1.x + acc1.y);
 }
 
+// d = t - s with s unpacked on the ALU pipe (SHF / LOP3) and one packed FFMA2 on the FMA pipe:
+// moves half of the per-element work off the FMA pipe (variant MS_SUB_UNPACK).
+__device__ __forceinline__ float2 sub_bf2_unpack(uint32_t x, float2 t) {
+  const float2 s = bf2_to_f2(x);
+  return __ffma2_rn(s, make_float2(-1.f, -1.f), t);
+}
+
+__device__ __forceinline__ float dist2_regs(const float2 (&T)[kR * 4], const uint4 (&x)[kR]) {
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+#if MS_SUB_UNPACK
+    const float2 d0 = sub_bf2_unpack(x[r].x, T[4 * r + 0]);
+    const float2 d1 = sub_bf2_unpack(x[r].y, T[4 * r + 1]);
+    const float2 d2 = sub_bf2_unpack(x[r].z, T[4 * r + 2]);
+    const float2 d3 = sub_bf2_unpack(x[r].w, T[4 * r + 3]);
+#else
+    const float2 d0 = sub_bf2(x[r].x, T[4 * r + 0]);
+    const float2 d1 = sub_bf2(x[r].y, T[4 * r + 1]);
+    const float2 d2 = sub_bf2(x[r].z, T[4 * r + 2]);
+    const float2 d3 = sub_bf2(x[r].w, T[4 * r + 3]);
+#endif
+    acc0 = __ffma2_rn(d0, d0, acc0);
+    acc1 = __ffma2_rn(d1, d1, acc1);
+    acc0 = __ffma2_rn(d2, d2, acc0);
+    acc1 = __ffma2_rn(d3, d3, acc1);
+  }
+  return (acc0.x + acc0.y) + (acc1.x + acc1.y);
+}
+
+// Consumer loop of the single-target Euclidean kernel (the shipped configuration), software
+// pipelined with two register buffers (ping-pong, no register copies): the next stage is loaded
+// into one buffer while the other is evaluated, so the shared-memory loads overlap the FMA work.
+// Each stage is described by a 16-byte header the producer precomputes (output offset, bytes,
+// anchor / pair / stop), so the consumer does no index arithmetic.
+struct StageView {
+  int64_t out;
+  int32_t bytes, code;
+};
+
+__device__ __forceinline__ StageView view_of(const DistSmem& sm, int st) {
+  const int4 h = *reinterpret_cast<const int4*>(&sm.meta[st].hdr);
+  StageView v;
+  v.out = (int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x);
+  v.bytes = h.z;
+  v.code = h.w;
+  return v;
+}
+
+__device__ __forceinline__ void load_stage(const DistSmem& sm, int st, int tid, int bytes, uint4 (&dst)[kR]) {
+  const uint4* src = reinterpret_cast<const uint4*>(sm.ring[st]);
+  if (bytes == kStageBytes) {                       // full stage: no predicates
+#pragma unroll
+    for (int r = 0; r < kR; ++r) dst[r] = src[tid + r * kConsumers];
+  } else {
+    const int nchunk = bytes >> 4;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int c = tid + r * kConsumers;
+      dst[r] = c < nchunk ? src[c] : make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+}
+
+__device__ __forceinline__ void eval_stage(const DistArgs& a, const StageView& v, const uint4 (&x)[kR],
+                                           float2 (&T)[kR * 4], int warp, int lane) {
+  if (v.code & H_ANCHOR) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      T[4 * r + 0] = bf2_to_f2(x[r].x);
+      T[4 * r + 1] = bf2_to_f2(x[r].y);
+      T[4 * r + 2] = bf2_to_f2(x[r].z);
+      T[4 * r + 3] = bf2_to_f2(x[r].w);
+    }
+  } else if (v.code & H_PAIR) {
+    const float s = warp_sum(dist2_regs(T, x));
+    if (lane == 0) a.ws.wpart[v.out + warp] = s;
+  }
+}
+
+__device__ __forceinline__ void consume_euclid(DistSmem& sm, const DistArgs& a, int tid, int warp, int lane) {
+  float2 T[kR * 4];
+  uint4 xa[kR], xb[kR];
+  int stage = 0;
+  uint32_t ph = 0;
+  auto advance = [&]() { if (++stage == kStages) { stage = 0; ph ^= 1u; } };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    advance();
+  };
+  mbar_wait(&sm.full[stage], ph);
+  StageView va = view_of(sm, stage), vb;
+  if (va.code & H_STOP) return;
+  load_stage(sm, stage, tid, va.bytes, xa);
+  release();
+  for (;;) {
+    mbar_wait(&sm.full[stage], ph);
+    vb = view_of(sm, stage);
+    if (!(vb.code & H_STOP)) load_stage(sm, stage, tid, vb.bytes, xb);
+    eval_stage(a, va, xa, T, warp, lane);            // overlaps the loads of xb
+    if (vb.code & H_STOP) break;
+    release();
+    mbar_wait(&sm.full[stage], ph);
+    va = view_of(sm, stage);
+    if (!(va.code & H_STOP)) load_stage(sm, stage, tid, va.bytes, xa);
+    eval_stage(a, vb, xb, T, warp, lane);
+    if (va.code & H_STOP) break;
+    release();
+  }
+}
+
 template <int kMetric>
 __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -566,6 +691,9 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
                       m.pair[0] = q < 0 ? (int32_t)cur.t : cur.lo + c0 + q;   // target slot: target index
                       m.anc[0] = 0;
                       m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes; m.flags = 0;
+                      const int64_t po = q < 0 ? 0 : (int64_t)(cur.lo + c0 + q);
+                      m.hdr = make_hdr((((po * a.N + l) * 2 + kv) * a.n_sub + sub) * kConsumerWarps, bytes,
+                                       q < 0 ? H_ANCHOR : H_PAIR);
                       mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
                       bulk_g2s(sm.ring[stage], base + (int64_t)phys * a.block_stride_b + boff, (uint32_t)bytes,
                                &sm.full[stage]);
@@ -587,6 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
       if (lane == 0) {
         mbar_wait(&sm.empty[stage], ph ^ 1u);
         sm.meta[stage].flags = F_STOP;
+        sm.meta[stage].hdr = make_hdr(0, 0, H_STOP);
         sm.meta[stage].nent = 0;
         sm.meta[stage].anchor = -1;
         mbar_arrive(&sm.full[stage]);
@@ -699,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
                 for (int e = 0; e < kMetaEnt; ++e) { m.pair[e] = t.pair[e]; m.anc[e] = t.anc[e]; }
                 m.nent = t.nent; m.anchor = t.anchor;
                 m.layer = l; m.kv = kv; m.sub = sub; m.bytes = bytes; m.flags = 0;
+                m.hdr = make_hdr(0, bytes, 0);    // the multi-anchor path uses the generic consumer
                 mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
                 bulk_g2s(sm.ring[stage], base + (int64_t)t.phys * a.block_stride_b + boff, (uint32_t)bytes,
                          &sm.full[stage]);
@@ -717,6 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
     if (lane == 0) {
       mbar_wait(&sm.empty[stage], ph ^ 1u);
       sm.meta[stage].flags = F_STOP;
+      sm.meta[stage].hdr = make_hdr(0, 0, H_STOP);
       sm.meta[stage].nent = 0;
       sm.meta[stage].anchor = -1;
       mbar_arrive(&sm.full[stage]);
@@ -725,6 +856,12 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
   }
 
   // -------------------------------------------------------------------- consumer warps
+#if MS_PIPE && MS_ANCHOR_FP32 && !MS_DIAG_NO_COMPUTE
+  if (kMetric == MEMSHARE_METRIC_EUCLIDEAN && kAnchors == 1) {
+    consume_euclid(sm, a, tid, warp, lane);
+    return;
+  }
+#endif
   AnchorT A[kAnchors];
   int stage = 0;
   uint32_t ph = 0;
