@@ -175,6 +175,8 @@ __device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {
 }
 
 __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ int2 s_tab[];                         // [kSmemSlots]
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
@@ -459,6 +461,8 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
 }
 
 __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -615,6 +619,8 @@ struct FillSmem {
 };
 
 __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FillSmem& sm = *reinterpret_cast<FillSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -761,8 +767,8 @@ extern "C" memshare_status memshare_step_candidates(
   const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
   const int grid_s1 = (int)(gcap < sms ? gcap : sms);      // 1024-thread CTAs: one per SM, one wave
-  encode_kernel<<<grid_enc, kNT, kSmemSlots * sizeof(int2), st>>>(a);
-  stage1_kernel<<<grid_s1, kNT1, sizeof(SelSmem), st>>>(a);
-  fill_kernel<<<grid_sel, kNT, sizeof(FillSmem), st>>>(a);
+  launch_pdl(encode_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
+  launch_pdl(stage1_kernel, dim3(grid_s1), dim3(kNT1), sizeof(SelSmem), st, a);
+  launch_pdl(fill_kernel, dim3(grid_sel), dim3(kNT), sizeof(FillSmem), st, a);
   return launch_status();
 }

@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "memshare.h"
@@ -114,6 +116,41 @@ __device__ void cta_scan_counts(const int32_t* cnt, int64_t* out_off, int64_t n,
     carry += tot;
   }
   if (threadIdx.x == 0) out_off[n] = carry;
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the path is launched with programmatic stream serialization (PDL): the next
+// kernel's CTAs may be scheduled while the previous kernel drains, and each kernel calls
+// pdl_wait() (griddepcontrol.wait: the predecessor grid has completed and its writes are
+// visible) before it touches any memory another kernel wrote or reads. pdl_trigger()
+// (griddepcontrol.launch_dependents) lets the successor launch early. Both are no-ops when the
+// kernel was launched without the attribute. MEMSHARE_PDL=0 disables the attribute (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MEMSHARE_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline int sm_count() {

@@ -365,6 +365,8 @@ __device__ void write_solo(const DistArgs& a, int64_t t, int64_t P, int64_t at) 
 }
 
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(DistArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ unsigned long long keys[];           // [pow2(T)] when T <= kPlanSortCap
   __shared__ int64_t sh[kPlanThreads / 32 + 1];
   const int tid = threadIdx.x;
@@ -497,12 +499,14 @@ __device__ __forceinline__ float dist2_anchor(const AnchorT (&A)[kAnchors], cons
   return (acc0.x + acc0.y) + (acc1.x + acc1.y);
 }
 
+#if MS_SUB_UNPACK
 // d = t - s with s unpacked on the ALU pipe (SHF / LOP3) and one packed FFMA2 on the FMA pipe:
 // moves half of the per-element work off the FMA pipe (variant MS_SUB_UNPACK).
 __device__ __forceinline__ float2 sub_bf2_unpack(uint32_t x, float2 t) {
   const float2 s = bf2_to_f2(x);
   return __ffma2_rn(s, make_float2(-1.f, -1.f), t);
 }
+#endif
 
 __device__ __forceinline__ float dist2_regs(const float2 (&T)[kR * 4], const uint4 (&x)[kR]) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
@@ -623,6 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();                       // setup above overlaps the predecessor's tail
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------------ producer warp
@@ -965,6 +971,8 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
 // streaming kernel left in the workspace (kernel boundary = the only synchronisation needed);
 // FINALIZE reads partial squared sums already reduced across ranks.
 __global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int from_partial) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double terms[kConsumers];
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
   for (int64_t t = blockIdx.x; t < T; t += gridDim.x)
@@ -1063,7 +1071,7 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   const int64_t tc = target_cap < 1 ? 1 : target_cap;
   const int fin_grid = (int)(tc < 8 * sm_count() ? tc : 8 * sm_count());
   if (mode == MEMSHARE_DIST_FINALIZE) {
-    finalize_kernel<<<fin_grid, kConsumers, 0, st>>>(a, 1);
+    launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 1);
     return launch_status();
   }
   static bool attr_set = false;
@@ -1080,11 +1088,11 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   if (cudaMemsetAsync(a.ws.ticket, 0, sizeof(unsigned int), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   int64_t plan_np2 = 1;
   while (plan_np2 < target_cap && plan_np2 < kPlanSortCap) plan_np2 <<= 1;
-  if (kAnchors > 1) plan_kernel<<<1, kPlanThreads, (size_t)plan_np2 * sizeof(unsigned long long), st>>>(a);
+  if (kAnchors > 1) launch_pdl(plan_kernel, dim3(1), dim3(kPlanThreads), (size_t)plan_np2 * sizeof(unsigned long long), st, a);
   if (metric == MEMSHARE_METRIC_COSINE)
-    distance_kernel<MEMSHARE_METRIC_COSINE><<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
+    launch_pdl(distance_kernel<MEMSHARE_METRIC_COSINE>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
   else
-    distance_kernel<MEMSHARE_METRIC_EUCLIDEAN><<<sm_count(), kThreads, sizeof(DistSmem), st>>>(a);
-  finalize_kernel<<<fin_grid, kConsumers, 0, st>>>(a, 0);
+    launch_pdl(distance_kernel<MEMSHARE_METRIC_EUCLIDEAN>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
+  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 0);
   return launch_status();
 }

@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(kNT) remap_kernel(int32_t* __restrict__ table,
                                                     const int64_t* __restrict__ num_targets, int64_t target_cap,
                                                     int32_t block_size, int64_t* __restrict__ num_freed,
                                                     int64_t* __restrict__ affected, RemapWs ws, int32_t* status) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int64_t sh[kNT / 32 + 1];
   __shared__ int bad;
   int64_t T = *num_targets;
@@ -144,7 +146,7 @@ extern "C" memshare_status memshare_remap(int32_t* block_table, int32_t table_st
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(ws.last_dec, 0xFF, sizeof(int32_t) * ((size_t)num_blocks + 1), st) != cudaSuccess)
     return MEMSHARE_ERR_CUDA;
-  remap_kernel<<<1, kNT, 0, st>>>(block_table, table_stride, num_seqs, refcount, num_blocks, free_list, free_count,
+  launch_pdl(remap_kernel, dim3(1), dim3(kNT), 0, st, block_table, table_stride, num_seqs, refcount, num_blocks, free_list, free_count,
                                   decisions, num_targets, target_cap, block_size, num_freed, affected_tokens, ws,
                                   device_status);
   return launch_status();

@@ -156,6 +156,8 @@ __device__ __forceinline__ Agg ld_agg(const int4* p) {
 }
 
 __global__ void __launch_bounds__(kNT) seg_kernel(SegArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ Agg s_warp[kNT / 32];
   __shared__ Agg s_tile_prefix;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -344,6 +346,6 @@ extern "C" memshare_status memshare_segment_steps(const int32_t* tokens, int64_t
   const int64_t tiles = (num_tokens + kTile - 1) / kTile;
   if (tiles > 0 && cudaMemsetAsync(a.ws.flag, 0, (size_t)tiles * sizeof(int32_t), st) != cudaSuccess)
     return MEMSHARE_ERR_CUDA;
-  seg_kernel<<<(unsigned)(tiles < 1 ? 1 : tiles), kNT, 0, st>>>(a);
+  launch_pdl(seg_kernel, dim3((unsigned)(tiles < 1 ? 1 : tiles)), dim3(kNT), 0, st, a);
   return launch_status();
 }
