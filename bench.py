@@ -32,7 +32,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "candidate KV-block pairs scored/s"
 UNIT = "pairs/s"
-GPU_LAUNCHES_PER_STEP = 9     # seg_count, seg_fill, seg_final, encode, stage1, fill, distance, finalize, remap
+GPU_LAUNCHES_PER_STEP = 7     # seg, encode, stage1, fill, distance, finalize, remap (our kernels; + 3 memset nodes)
 
 
 def parse():

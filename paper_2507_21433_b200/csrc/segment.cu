@@ -1,8 +1,9 @@
 // a1 -- step segmentation (readings R1-R4).
 //
 // ONE single-pass kernel over the FLAT token array (sequences are concatenated, so the global
-// order of step ends is the global step order). Each CTA owns a 4096-token tile and computes,
-// per thread of 4 tokens, an aggregate (ends, content, last boundary): a "boundary" is the
+// order of step ends is the global step order). Each CTA owns a kTile-token tile (1024 threads x 4
+// tokens; larger per-thread runs were measured slower: their loads do not coalesce) and computes,
+// per thread of kItems tokens, an aggregate (ends, content, last boundary): a "boundary" is the
 // position where the next step starts -- a sequence's generation start, or the token after a
 // step end -- together with the content-token prefix at that point. Aggregates combine with an
 // associative operator (counts add; the later boundary wins), so a block scan gives each
@@ -19,8 +20,15 @@
 namespace ms {
 namespace {
 
-constexpr int kNT = 1024;
-constexpr int kItems = 4;
+#ifndef MS_SEG_NT
+#define MS_SEG_NT 1024
+#endif
+#ifndef MS_SEG_ITEMS
+#define MS_SEG_ITEMS 4
+#endif
+constexpr int kNT = MS_SEG_NT;           // threads per tile
+constexpr int kItems = MS_SEG_ITEMS;     // tokens per thread (a 32-bit flag word each)
+static_assert(kItems <= 32, "per-thread flags are 32-bit masks");
 constexpr int kTile = kNT * kItems;
 
 // (ends, content, bpos, bcb): bpos = position (flat) of the last boundary or -1, bcb = content
@@ -198,13 +206,13 @@ __global__ void __launch_bounds__(kNT) seg_kernel(SegArgs a) {
   if (lane == 31) s_warp[w] = x;
   __syncthreads();
   if (w == 0) {
-    Agg v = s_warp[lane];
+    Agg v = lane < kNT / 32 ? s_warp[lane] : agg_identity();
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const Agg y = shfl_agg_up(v, o);
       if (lane >= o) v = combine(y, v);
     }
-    s_warp[lane] = v;                                    // inclusive warp totals
+    if (lane < kNT / 32) s_warp[lane] = v;               // inclusive warp totals
   }
   __syncthreads();
   Agg excl = shfl_agg_up(x, 1);
