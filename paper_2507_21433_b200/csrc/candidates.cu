@@ -34,7 +34,7 @@ constexpr int kSmemSlots = 8192;       // smem hash table (steps with <= 2048 co
 constexpr int kCandCap = 1024;         // survivors held per current step
 constexpr int kChunk = kCandCap / 2;   // history steps per selection chunk
 constexpr int kMaxTgt = 4096;          // full blocks per step handled by the fill kernel
-constexpr int kHistTok = 12288;        // history tokens staged in smem per pass (48 KiB)
+constexpr int kHistTok = 16384;        // history tokens staged in smem per pass (64 KiB)
 constexpr int32_t kEmpty = -1;
 
 struct CandWs {
@@ -460,7 +460,7 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
   if (threadIdx.x == 0) { a.ws.off_m[G] = cm; a.ws.off_t[G] = ct; a.ws.off_p[G] = cp; }
 }
 
-__global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
+__global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -500,6 +500,8 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       }
       __syncthreads();
       if (jb == 0) DBG_T(10);
+      if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
+        g_dbg_t[blockIdx.x * kDbgSlots + 12] = clock64();
       const int32_t lo = sm.hst[0], hi = sm.hen[nj - 1];
       for (int32_t clo = lo; clo < hi; clo += kHistTok) {
         const int32_t chi = (hi - clo > kHistTok) ? clo + kHistTok : hi;
@@ -519,6 +521,8 @@ __global__ void __launch_bounds__(kNT1) stage1_kernel(CandArgs a) {
       }
       __syncthreads();
       if (jb == 0) DBG_T(11);
+      if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
+        g_dbg_t[blockIdx.x * kDbgSlots + 13] = clock64();
       for (int i = threadIdx.x; i < nj; i += kNT1) {
         const int64_t gj = gfirst + jb + i;
         if (a.step_nbag[gj] == 0) continue;                // void history step (reading R5)

@@ -163,7 +163,7 @@ __device__ __forceinline__ Agg ld_agg(const int4* p) {
   return Agg{v.x, v.y, v.z, v.w};
 }
 
-__global__ void __launch_bounds__(kNT) seg_kernel(SegArgs a) {
+__global__ void __launch_bounds__(kNT, 1) seg_kernel(SegArgs a) {
   pdl_trigger();
   pdl_wait();
   __shared__ Agg s_warp[kNT / 32];

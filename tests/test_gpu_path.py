@@ -208,6 +208,41 @@ def test_distance_properties_on_gpu():
     compare_distances(D, Do)
 
 
+def test_head_sharded_two_shards_on_one_gpu():
+    """KV-head sharding (bench.py --mode headshard) with both shards on this
+    GPU: each shard holds 4 of the 8 KV heads, runs a1-a4 (identical pair lists) and PARTIAL;
+    the device-side sum of the partial squared sums stands in for the NCCL all-reduce; FINALIZE
+    with the global h must match the fp64 oracle on the full 8-head pool."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    shape = kv.KVShape(4, 8, 128, 16)
+    w = workloads.small(shape, 2, 4000, seed=11)
+    shards = [make_path(w, h_local=4, head_offset=h0) for h0 in (0, 4)]
+    for p in shards:
+        p.autosize(w.tau_s)
+        p.segment()
+        p.candidates(w.tau_s)
+        p.alloc_partial()
+        p.distance_call(w.tau_b, L.DIST_PARTIAL)
+    torch.cuda.synchronize()
+    c0, c1 = (p.read_candidates() for p in shards)
+    for k_ in c0["pairs"]:
+        assert np.array_equal(c0["pairs"][k_], c1["pairs"][k_]), k_
+    p = shards[0]
+    p.partial_sq += shards[1].partial_sq                   # the all-reduce (sum over head shards)
+    p.distance_call(w.tau_b, L.DIST_FINALIZE)
+    torch.cuda.synchronize()
+    assert p.read_status() == 0 and shards[1].read_status() == 0
+    gd = p.read_distance()
+    pr = c0["pairs"]
+    kh, vh, ls, bs = w.host_pool()
+    D = oracle.block_distance(kh, vh, ls, bs, shape.num_layers, shape.num_kv_heads, shape.num_kv_heads,
+                              shape.head_dim, shape.block_size, pr["target_phys"], pr["source_phys"])
+    assert pr["seq"].size > 0
+    compare_distances(gd["distance"], D)
+    compare_decisions(gd["decisions"], D, c0["target_off"], pr["source_logical"], w.tau_b)
+
+
 def test_partial_then_finalize_equals_full():
     import torch
     from paper_2507_21433_b200 import _lib as L
