@@ -43,6 +43,14 @@ def peak():
 
 PEAK = peak()
 FLUSH = None
+# CUDA-core ceiling of the distance inner loop (one FHFMA.BF16 + half an FFMA2 per bf16 element
+# pair), measured on this pool's B200 by scripts/alu_peak.cu (registers only, 16-64 warps/SM)
+ALU_PEAK = 13.4e12
+
+
+def EP(sh):
+    """element pairs per block pair (K and V, all layers)"""
+    return sh.num_layers * 2 * sh.block_size * sh.num_kv_heads * sh.head_dim
 
 
 def flush_l2():
@@ -122,7 +130,8 @@ def row_f2_cross(rows):
         slices = P + int(p.counts()["targets"])
         emit("f2 CROSS pairing distance", workload="c2 cross", pairs=P, distinct_blocks=U, bytes=byts, us=t,
              pairs_per_s=P / (t * 1e-6), slice_reads_per_layer=slices,
-             ingest_GBps=round(slices * sh.num_layers * 2 * 32768 / (t * 1e-6) / 1e9, 1))
+             ingest_GBps=round(slices * sh.num_layers * 2 * 32768 / (t * 1e-6) / 1e9, 1),
+             elem_pairs_per_s=P * EP(sh) / (t * 1e-6), frac_of_alu_peak=round(P * EP(sh) / (t * 1e-6) / ALU_PEAK, 4))
     if "f4" in rows:
         p.set_caps(Caps(step=p.caps.step, match=max(1024, p.num_tokens), pair=p.caps.pair, target=p.caps.target))
         p.segment()
@@ -148,6 +157,7 @@ def row_f3(rows):
     assert p.read_status() == 0
     emit("f3 all-pairs block matrix", workload=f"c2 window of {Wn} blocks", pairs=P, distinct_blocks=U, bytes=byts,
          us=t, pairs_per_s=P / (t * 1e-6), all_pairs_enum_us=t_ap,
+         elem_pairs_per_s=P * EP(sh) / (t * 1e-6), frac_of_alu_peak=round(P * EP(sh) / (t * 1e-6) / ALU_PEAK, 4),
          note="bytes = distinct blocks once; every source is re-read from L2 by later targets")
     del p
     torch.cuda.empty_cache()
