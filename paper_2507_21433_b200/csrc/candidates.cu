@@ -21,6 +21,8 @@
 #include <climits>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace ms {
@@ -466,16 +468,36 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // Thread-block cluster of csize CTAs per current step (online rounds: few current steps, long
+  // histories): every rank builds the step's table, streams 1/csize of the history into its own
+  // shared dot array, and rank 0 sums the ranks' arrays over DSMEM and does the selection.
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+  const int64_t cid = blockIdx.x / csize, ncl = gridDim.x / csize;
   DBG_T(0);
   const int64_t G = total_steps(a);
-  for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+  // LAST (online): the work list is one step per sequence, found directly; the counts of every
+  // other step are zeroed up front by all threads (one parallel pass instead of a chain of
+  // dependent loads per skipped step).
+  const bool last_mode = a.cur_mode == MEMSHARE_CUR_LAST;
+  if (last_mode) {
+    for (int64_t g = (int64_t)blockIdx.x * kNT1 + threadIdx.x; g < G; g += (int64_t)gridDim.x * kNT1) {
+      const int32_t s = a.ws.step_seq[g];
+      if (g != a.seq_step_off[s + 1] - 1) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
+    }
+  }
+  const int64_t nwork = last_mode ? a.num_seqs : G;
+  for (int64_t wi = cid; wi < nwork; wi += ncl) {
+    const int64_t g = last_mode ? a.seq_step_off[wi + 1] - 1 : wi;
+    if (last_mode && (g < a.seq_step_off[wi] || g >= G)) continue;   // sequence without steps
     const int32_t s = a.ws.step_seq[g];
     const int64_t gfirst = a.seq_step_off[s];
     const int64_t S = a.seq_step_off[s + 1] - gfirst;
     const int64_t k = g - gfirst;
     const int32_t nbag = a.step_nbag[g];
     if (nbag == 0 || !is_current(a, s, k, S)) {
-      if (threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
+      if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
       continue;
     }
     const int64_t tok_base = a.seq_tok_off[s];
@@ -502,7 +524,9 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
       if (jb == 0) DBG_T(10);
       if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
         g_dbg_t[blockIdx.x * kDbgSlots + 12] = clock64();
-      const int32_t lo = sm.hst[0], hi = sm.hen[nj - 1];
+      const int32_t lo0 = sm.hst[0], hi0 = sm.hen[nj - 1];
+      const int32_t lo = lo0 + (int32_t)((int64_t)(hi0 - lo0) * crank / csize);      // this rank's share
+      const int32_t hi = lo0 + (int32_t)((int64_t)(hi0 - lo0) * (crank + 1) / csize);
       for (int32_t clo = lo; clo < hi; clo += kHistTok) {
         const int32_t chi = (hi - clo > kHistTok) ? clo + kHistTok : hi;
         // coalesced, independent loads: one memory latency for the whole pass
@@ -520,6 +544,23 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
         __syncthreads();
       }
       __syncthreads();
+      if (csize > 1) {
+        cl.sync();                                         // every rank's partial dots are final
+        if (crank == 0) {
+          for (int i = threadIdx.x; i < nj; i += kNT1) {
+            uint64_t d = ((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i];
+            for (int r = 1; r < csize; ++r) {
+              const uint32_t* rl = cl.map_shared_rank(sm.dot_lo, r);
+              const uint32_t* rh = cl.map_shared_rank(sm.dot_hi, r);
+              d += ((uint64_t)rh[i] << 32) | rl[i];
+            }
+            sm.dot_lo[i] = (uint32_t)d;
+            sm.dot_hi[i] = (uint32_t)(d >> 32);
+          }
+        }
+        cl.sync();                                         // remote reads done before ranks reuse them
+        if (crank != 0) continue;                          // ranks > 0 only stream (uniform per CTA)
+      }
       if (jb == 0) DBG_T(11);
       if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
         g_dbg_t[blockIdx.x * kDbgSlots + 13] = clock64();
@@ -543,6 +584,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
         __syncthreads();
       }
     }
+    if (crank != 0) continue;
     DBG_T(2);
     if (sm.overflow) {
       if (threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
@@ -770,9 +812,36 @@ extern "C" memshare_status memshare_step_candidates(
   const int64_t gcap = step_cap < 1 ? 1 : step_cap;
   const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
-  const int grid_s1 = (int)(gcap < sms ? gcap : sms);      // 1024-thread CTAs: one per SM, one wave
   launch_pdl(encode_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
-  launch_pdl(stage1_kernel, dim3(grid_s1), dim3(kNT1), sizeof(SelSmem), st, a);
+  {
+    // cluster size per current step: online rounds (LAST: one current step per sequence) split
+    // each step's history over up to 8 CTAs while the clusters still fit in one wave; offline
+    // (ALL) and RANGE calls keep one CTA per step. MEMSHARE_S1_CLUSTER overrides (tuning).
+    static int env_cs = -1;
+    if (env_cs < 0) { const char* e = getenv("MEMSHARE_S1_CLUSTER"); env_cs = e ? atoi(e) : 0; }
+    int cs = 1;
+    if (env_cs > 0) cs = env_cs;
+    else if (cur_mode == MEMSHARE_CUR_LAST)
+      for (int c = 8; c > 1; c >>= 1)
+        if ((int64_t)num_seqs * c <= sms) { cs = c; break; }
+    if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
+    const int ncl = (int)((gcap < sms / cs) ? gcap : sms / cs);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ncl * cs));
+    cfg.blockDim = dim3(kNT1);
+    cfg.dynamicSmemBytes = sizeof(SelSmem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)cs;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, stage1_kernel, a) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  }
   launch_pdl(fill_kernel, dim3(grid_sel), dim3(kNT), sizeof(FillSmem), st, a);
   return launch_status();
 }

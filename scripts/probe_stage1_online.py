@@ -35,9 +35,14 @@ L.lib.memshare_debug_stage1_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert L.lib.memshare_debug_stage1_times(buf.ctypes.data, buf.size) == 0
 t = buf.reshape(2048, 16).astype(np.int64)
 G = int(path.seq_step_off[-1].item())
-n = min(G, 148)
+cs = int(os.environ.get("CS", "8"))
+ncl = 148 // cs
+n = ncl * cs
 t0 = t[:n, 0].min()
-owner = (G - 1) % n
+owner = 0                                    # LAST mode: sequence 0 -> cluster 0
+for r in range(cs):
+    rr = (t[owner + r] - t0) / 1e3
+    print(f"rank {r}: start {rr[0]:.2f} table {rr[1]:.2f} staged {rr[10]:.2f} loop-end {rr[7]:.2f}")
 r = (t[owner] - t0) / 1e3
 names = {0: "start", 1: "table", 10: "hist staged", 11: "stream done", 2: "select", 3: "sort", 4: "stash",
          5: "prepare", 6: "count", 7: "loop end"}

@@ -90,9 +90,18 @@ def test_stage1_and_pair_variants(tau_s, top_k, pairing):
 
 
 def test_online_modes():
+    """LAST with 3 sequences runs Stage 1 as 8-CTA clusters per current step (DSMEM sum of the
+    ranks' partial dots); RANGE runs one CTA per step."""
     w = workloads.small(SMALL, 3, 3000, seed=3)
     full_parity(w, cur_mode=oracle.CUR_LAST)
     full_parity(w, cur_mode=oracle.CUR_RANGE, cb=[0, 5, 10], ce=[4, 30, 11])
+
+
+@pytest.mark.parametrize("num_seqs", [20, 40, 100])
+def test_online_last_cluster_sizes(num_seqs):
+    """LAST rounds over many sequences: Stage-1 clusters of 4, 2 and 1 CTAs per current step."""
+    w = workloads.small(SMALL, num_seqs, 900, seed=num_seqs, gen_start=16)
+    full_parity(w, tau_s=0.5, cur_mode=oracle.CUR_LAST)
 
 
 def test_qwen32b_shape_two_sequences():
