@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c2", choices=["c2", "tiny", "c3", "c4"])
     ap.add_argument("--seqs-per-gpu", type=int, default=0, help="c3/c4: sequences per GPU (0 = config default)")
+    ap.add_argument("--wave", type=int, default=0,
+                    help="c3: which wave of the batch (rank r of N holds sequences (wave*N + r)*seqs ...); a "
+                         "64-sequence batch on 1 GPU is waves 0 and 1 of 32")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="seq", choices=["seq", "headshard"])
     ap.add_argument("--seed", type=int, default=int(os.environ.get("MEMSHARE_SEED", "0")))
@@ -60,14 +63,14 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def make_workload(cfg, seed, rank, seqs):
+def make_workload(cfg, seed, rank, seqs, wave=0, world=1):
     from synth import workloads
     if cfg == "c2":
         return workloads.c2(seed=seed + rank)
     if cfg == "tiny":
         return workloads.tiny(eta=0.05)
     if cfg == "c3":
-        return workloads.c3(num_seqs=seqs or 8, seed=seed, first_seq=rank * (seqs or 8))
+        return workloads.c3(num_seqs=seqs or 8, seed=seed, first_seq=(wave * world + rank) * (seqs or 8))
     if cfg == "c4":
         return workloads.c4(num_seqs=seqs or 8, seed=seed + rank)
     raise ValueError(cfg)
@@ -85,7 +88,8 @@ def describe(cfg, w, world, mode):
             "seqs_per_gpu": w.batch.num_seqs, "tokens_per_gpu": w.num_tokens, "tau_s": w.tau_s,
             "tau_b": round(w.tau_b, 6), "eta": w.eta, "pairing": "aligned", "stage1": "offline (every step current)",
             "parallelism": (f"seq-shard dp{world}" if mode == "seq" else f"kv-head-shard hs{world}"),
-            "l2": "inputs larger than L2 (pool %.2f GB/GPU vs 126 MB L2); no flush" % (w.pool_bytes() / 1e9)}
+            "l2": "inputs larger than L2 (pool %.2f GB/GPU vs 126 MB L2); no flush" % (w.pool_bytes() / 1e9),
+            **({"first_seq": int(getattr(w, "first_seq", 0))} if cfg == "c3" else {})}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -199,7 +203,7 @@ def run_reference(args, rank, world):
         return
     import oracle
     oracle.build()
-    w = make_workload(args.config, args.seed, 0, args.seqs_per_gpu)
+    w = make_workload(args.config, args.seed, 0, args.seqs_per_gpu, args.wave)
     k, v, ls, bs = w.host_pool()
     sh = w.shape
     st = oracle.segment_steps(w.batch.tokens, w.batch.seq_tok_off, w.batch.gen_start, w.batch.final, w.batch.delim_ids)
@@ -264,7 +268,8 @@ def main():
     from paper_2507_21433_b200 import _lib as L
     from paper_2507_21433_b200.pipeline import MemSharePath
 
-    w = make_workload(args.config, args.seed, rank if args.mode == "seq" else 0, args.seqs_per_gpu)
+    w = make_workload(args.config, args.seed, rank if args.mode == "seq" else 0, args.seqs_per_gpu, args.wave,
+                      world if args.mode == "seq" else 1)
     sh = w.shape
     h_local, h_off = sh.num_kv_heads, 0
     if args.mode == "headshard":

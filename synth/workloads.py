@@ -100,7 +100,9 @@ def c2(seed: int = 0, eta: float = 0.05, tau_s: float = 0.8) -> Workload:
 def c3(num_seqs: int = 64, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8, first_seq: int = 0) -> Workload:
     """configs[2]: QwQ-32B KV shape, batch of 12,288-token CoTs (a slice of the 64 for waves)."""
     b = traces.make_batch(seed * 1000 + first_seq, num_seqs, 12288, 128, kv.QWEN32B.block_size)
-    return _paged(f"c3_qwq32b_{num_seqs}x12288", kv.QWEN32B, b, seed, eta, tau_s)
+    w = _paged(f"c3_qwq32b_{num_seqs}x12288", kv.QWEN32B, b, seed, eta, tau_s)
+    w.first_seq = first_seq
+    return w
 
 
 def c4(num_seqs: int = 128, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8) -> Workload:
