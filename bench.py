@@ -40,10 +40,10 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="c2", choices=["c2", "tiny", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "tiny", "c3", "c4", "c5"])
     ap.add_argument("--seqs-per-gpu", type=int, default=0, help="c3/c4: sequences per GPU (0 = config default)")
     ap.add_argument("--wave", type=int, default=0,
-                    help="c3: which wave of the batch (rank r of N holds sequences (wave*N + r)*seqs ...); a "
+                    help="c3/c5: which wave of the batch (rank r of N holds sequences (wave*N + r)*seqs ...); a "
                          "64-sequence batch on 1 GPU is waves 0 and 1 of 32")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="seq", choices=["seq", "headshard"])
@@ -73,6 +73,8 @@ def make_workload(cfg, seed, rank, seqs, wave=0, world=1):
         return workloads.c3(num_seqs=seqs or 8, seed=seed, first_seq=(wave * world + rank) * (seqs or 8))
     if cfg == "c4":
         return workloads.c4(num_seqs=seqs or 8, seed=seed + rank)
+    if cfg == "c5":
+        return workloads.c5(num_seqs=seqs or 32, seed=seed, first_seq=(wave * world + rank) * (seqs or 32))
     raise ValueError(cfg)
 
 
@@ -82,14 +84,16 @@ def describe(cfg, w, world, mode):
                                 "per GPU (128-token prompt, MATH-500-like planted redundancy)",
                          "tiny": "configs[0]: tiny T0 fixture",
                          "c3": "configs[2]: QwQ-32B KV shape, 12,288-token CoTs",
-                         "c4": "configs[3]: Phi-4-reasoning-plus KV shape, AIME-length traces"}[cfg],
+                         "c4": "configs[3]: Phi-4-reasoning-plus KV shape, AIME-length traces",
+                         "c5": "configs[4]: 32B KV shape, 16,384-token CoTs (512 over 8 GPUs = 2 waves of 32 per "
+                               "GPU; this line is one wave)"}[cfg],
             "kv_shape": {"layers": sh.num_layers, "kv_heads": sh.num_kv_heads, "head_dim": sh.head_dim,
                          "block_size": sh.block_size, "kv_dtype": "bf16"},
             "seqs_per_gpu": w.batch.num_seqs, "tokens_per_gpu": w.num_tokens, "tau_s": w.tau_s,
             "tau_b": round(w.tau_b, 6), "eta": w.eta, "pairing": "aligned", "stage1": "offline (every step current)",
             "parallelism": (f"seq-shard dp{world}" if mode == "seq" else f"kv-head-shard hs{world}"),
             "l2": "inputs larger than L2 (pool %.2f GB/GPU vs 126 MB L2); no flush" % (w.pool_bytes() / 1e9),
-            **({"first_seq": int(getattr(w, "first_seq", 0))} if cfg == "c3" else {})}
+            **({"first_seq": int(getattr(w, "first_seq", 0))} if cfg in ("c3", "c5") else {})}
 
 
 # ----------------------------------------------------------------------------- clocks

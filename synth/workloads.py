@@ -105,6 +105,15 @@ def c3(num_seqs: int = 64, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8,
     return w
 
 
+def c5(num_seqs: int = 32, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8, first_seq: int = 0) -> Workload:
+    """configs[4]: 32B KV shape, 512 x 16,384-token CoTs across 8 GPUs = 64 per GPU, run as waves of
+    32 (137 GB of KV per wave); this builds one wave (sequences first_seq .. first_seq + num_seqs)."""
+    b = traces.make_batch(seed * 1000 + 500 + first_seq, num_seqs, 16384, 128, kv.QWEN32B.block_size)
+    w = _paged(f"c5_32b_{num_seqs}x16384", kv.QWEN32B, b, seed, eta, tau_s)
+    w.first_seq = first_seq
+    return w
+
+
 def c4(num_seqs: int = 128, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8) -> Workload:
     """configs[3]: Phi-4-reasoning-plus KV shape, AIME-length traces L ~ U[8192, 16620]."""
     rng = np.random.default_rng(seed + 4)
