@@ -479,6 +479,19 @@ def main():
             out_dec.copy_(path.decisions, non_blocking=True)
             out_tab.copy_(path.table, non_blocking=True)
             out_cnt.copy_(cnt_dev, non_blocking=True)
+
+        e2e_body = e2e_step
+        e2e_graph = not args.no_graph and args.mode == "seq"
+        if e2e_graph:
+            # a serving loop replays the round as one CUDA graph: memcpy nodes read the pinned
+            # host inputs / write the pinned host outputs at replay time, the ABI calls in between
+            e2e_body()
+            torch.cuda.synchronize()
+            e2e_g = path.capture(e2e_body)
+            e2e_body = e2e_g.replay
+
+        def e2e_step():
+            e2e_body()
             torch.cuda.current_stream(dev).synchronize()
 
         for _ in range(max(3, args.warmup // 4)):
@@ -504,7 +517,9 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms, "steps": n_e2e,
                "note": "public API (MemSharePath over the C ABI); per step: pinned H2D of tokens/offsets/table/"
                        "refcounts/free list, the 4 calls, D2H of decisions/table/counters, stream sync; the KV pool "
-                       "is the device-resident serving cache"}
+                       "is the device-resident serving cache" + ("; the round (H2D + calls + D2H) is replayed as one "
+                       "CUDA graph captured through MemSharePath.capture, a host sync per step" if e2e_graph else
+                       "; calls launched eagerly")}
 
     # ---------------------------------------------------------------- cpu baseline (rank 0, N = 1)
     cpu = None
