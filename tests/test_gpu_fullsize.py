@@ -81,3 +81,8 @@ def test_c3_one_wave_32_sequences():
 
 def test_c4_phi4_32_sequences():
     sampled_parity(workloads.c4(num_seqs=32, seed=0))
+
+
+def test_c5_one_wave_32_sequences():
+    """configs[4]: 32 x 16,384-token CoTs at the 32B shape (one per-GPU wave, 137 GB pool)."""
+    sampled_parity(workloads.c5(num_seqs=32, seed=0))

@@ -367,6 +367,13 @@ def test_c2_full_size_parity():
           f"near_tie={near_tie}")
 
 
+def test_c2_full_size_online_round():
+    """configs[1] online: only the last finished step is current; Stage 1 runs as an
+    8-CTA cluster over its 12k-token history; everything bit-exact / within tolerance."""
+    w = workloads.c2(seed=1)
+    full_parity(w, cur_mode=oracle.CUR_LAST)
+
+
 COS_ATOL = 2e-6      # fp32 dot/norm sums of <= 2^14 bf16 products, cosine formed in fp64 (DESIGN.md R34)
 
 
