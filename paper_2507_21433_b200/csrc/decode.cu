@@ -109,24 +109,32 @@ __global__ void __launch_bounds__(kAppNT) append_alloc_kernel(int32_t* table, in
   if (threadIdx.x == 0) { *free_count = fc - need_total; *ws.ok = 1; }
 }
 
-// Copy the new K/V rows (h * d_h bf16 each, one per (layer, sequence)) into their slots.
-__global__ void append_copy_kernel(uint16_t* k, uint16_t* v, int64_t layer_stride, int64_t block_stride,
-                                   int32_t num_layers, int32_t num_seqs, int32_t row_elems, const uint16_t* new_k,
-                                   const uint16_t* new_v, AppWs ws) {
+// Copy the new K/V rows (h * d_h bf16 each, one per (layer, sequence)) into their slots. A warp
+// moves one row per iteration (16-byte vectors, K and V loads issued together, 32-bit index
+// math: the row index is split once per row, not per vector).
+__global__ void __launch_bounds__(256) append_copy_kernel(uint16_t* k, uint16_t* v, int64_t layer_stride,
+                                                          int64_t block_stride, int32_t num_layers, int32_t num_seqs,
+                                                          int32_t row_elems, const uint16_t* new_k,
+                                                          const uint16_t* new_v, AppWs ws) {
   if (__ldcg(ws.ok) == 0) return;
-  const int vec = row_elems / 8;                 // 16-byte vectors per row
-  const int64_t total = (int64_t)num_layers * num_seqs * vec;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vec;
-    const int c = (int)(i % vec);
-    const int32_t l = (int32_t)(r / num_seqs), s = (int32_t)(r % num_seqs);
+  const int lane = threadIdx.x & 31;
+  const int32_t vec = row_elems / 8;             // 16-byte vectors per row
+  const int32_t rows = num_layers * num_seqs;
+  const int32_t warps = (int32_t)(gridDim.x * (blockDim.x / 32));
+  for (int32_t r = (int32_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)); r < rows; r += warps) {
+    const int32_t l = r / num_seqs, s = r - l * num_seqs;
     const int32_t b = __ldcg(ws.slot_blk + s);
     if (b < 0) continue;
-    const int64_t dst = (int64_t)l * layer_stride + (int64_t)b * block_stride +
-                        (int64_t)__ldcg(ws.slot_off + s) * row_elems + c * 8;
-    const int64_t src = r * row_elems + c * 8;
-    *reinterpret_cast<uint4*>(k + dst) = __ldg(reinterpret_cast<const uint4*>(new_k + src));
-    *reinterpret_cast<uint4*>(v + dst) = __ldg(reinterpret_cast<const uint4*>(new_v + src));
+    const int64_t dst = (int64_t)l * layer_stride + (int64_t)b * block_stride + (int64_t)__ldcg(ws.slot_off + s) * row_elems;
+    const uint4* sk = reinterpret_cast<const uint4*>(new_k + (int64_t)r * row_elems);
+    const uint4* sv = reinterpret_cast<const uint4*>(new_v + (int64_t)r * row_elems);
+    uint4* dk = reinterpret_cast<uint4*>(k + dst);
+    uint4* dv = reinterpret_cast<uint4*>(v + dst);
+    for (int32_t c = lane; c < vec; c += 32) {
+      const uint4 xk = __ldg(sk + c), xv = __ldg(sv + c);
+      dk[c] = xk;
+      dv[c] = xv;
+    }
   }
 }
 
@@ -438,8 +446,9 @@ extern "C" memshare_status memshare_kv_append(void* k_pool, void* v_pool, int64_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   append_alloc_kernel<<<1, kAppNT, 0, st>>>(block_table, table_stride, num_seqs, seq_len, active, refcount, num_blocks,
                                             free_list, free_count, d.block_size, ws, device_status);
-  const int64_t work = (int64_t)d.num_layers * num_seqs * (row / 8);
-  const int grid = (int)std::min<int64_t>((work + 255) / 256, 8 * sm_count());
+  const int64_t rows = (int64_t)d.num_layers * num_seqs;
+  if (rows > INT32_MAX) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  const int grid = (int)std::min<int64_t>((rows + 7) / 8, 8 * sm_count());    // 8 warps (rows) per CTA
   append_copy_kernel<<<grid, 256, 0, st>>>(static_cast<uint16_t*>(k_pool), static_cast<uint16_t*>(v_pool),
                                            layer_stride, block_stride, d.num_layers, num_seqs, (int32_t)row,
                                            static_cast<const uint16_t*>(new_k), static_cast<const uint16_t*>(new_v),
