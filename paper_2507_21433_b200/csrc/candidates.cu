@@ -801,7 +801,8 @@ extern "C" memshare_status memshare_step_candidates(
   a.ws = cand_layout(w, num_tokens, step_cap, match_cap);
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static bool attr_set = false;
+  static bool attr_set_dev[kMaxDevices] = {};
+  bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
     cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem));
     cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemSlots * sizeof(int2)));

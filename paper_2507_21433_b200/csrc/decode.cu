@@ -515,7 +515,8 @@ extern "C" memshare_status memshare_paged_attention_decode(
   a.pacc = w.take<float>(parts * d.head_dim);
   a.status = device_status;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static bool attr_set = false;
+  static bool attr_set_dev[kMaxDevices] = {};
+  bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
     cudaFuncSetAttribute(attn_split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)attn_smem_bytes<128>());

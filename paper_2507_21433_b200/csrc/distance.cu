@@ -1074,7 +1074,8 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
     launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 1);
     return launch_status();
   }
-  static bool attr_set = false;
+  static bool attr_set_dev[kMaxDevices] = {};
+  bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
     if (cudaFuncSetAttribute(distance_kernel<MEMSHARE_METRIC_EUCLIDEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(DistSmem)) != cudaSuccess ||
