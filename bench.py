@@ -47,6 +47,9 @@ def parse():
                          "64-sequence batch on 1 GPU is waves 0 and 1 of 32")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="seq", choices=["seq", "headshard"])
+    ap.add_argument("--collective", default="p2p", choices=["p2p", "nccl"],
+                    help="headshard, N>1: 'p2p' = FINALIZE reads every rank's partial sums over NVLink from "
+                         "symmetric memory (memshare_block_distance_finalize_peers); 'nccl' = all-reduce + FINALIZE")
     ap.add_argument("--seed", type=int, default=int(os.environ.get("MEMSHARE_SEED", "0")))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -287,6 +290,29 @@ def main():
     counts = path.autosize(w.tau_s)
     if args.mode == "headshard":
         path.alloc_partial()
+    # headshard across GPUs: the cross-rank reduction fused into FINALIZE over peer memory
+    symm_hdl, peer_ptrs, collective = None, None, ("none" if world == 1 or args.mode != "headshard" else args.collective)
+    if collective == "p2p":
+        try:
+            import torch.distributed._symmetric_memory as symm
+            buf = symm.empty(path.partial_sq.numel(), dtype=torch.float32, device=dev)
+            symm_hdl = symm.rendezvous(buf, dist.group.WORLD.group_name)
+            path.partial_sq = buf                      # PARTIAL writes into this rank's symmetric buffer
+            peer_ptrs = torch.tensor(list(symm_hdl.buffer_ptrs), dtype=torch.int64, device=dev)
+        except Exception as e:                         # no symmetric memory on this node: NCCL all-reduce
+            print(f"bench: symmetric memory unavailable ({e!r}); using the NCCL all-reduce", file=sys.stderr)
+            collective = "nccl"
+
+    def headshard_distance():
+        path.distance_call(w.tau_b, L.DIST_PARTIAL)
+        if collective == "p2p":
+            symm_hdl.barrier(channel=0)                # every rank's partial sums are written
+            path.finalize_peers(w.tau_b, peer_ptrs, world)
+            symm_hdl.barrier(channel=1)                # every rank has read them (buffer reusable)
+        else:
+            if collective == "nccl":
+                dist.all_reduce(path.partial_sq[:counts["pairs"] * sh.num_layers * 2])
+            path.distance_call(w.tau_b, L.DIST_FINALIZE)
     torch.cuda.synchronize()
     pristine = path.state.clone()
     stream = torch.cuda.current_stream(dev)
@@ -302,10 +328,7 @@ def main():
 
     def middle():                # a5-a6 (the HBM-bound kernel)
         if args.mode == "headshard":
-            path.distance_call(w.tau_b, L.DIST_PARTIAL)
-            if world > 1:
-                dist.all_reduce(path.partial_sq[:counts["pairs"] * sh.num_layers * 2])
-            path.distance_call(w.tau_b, L.DIST_FINALIZE)
+            headshard_distance()
         else:
             path.distance_call(w.tau_b)
 
@@ -315,7 +338,7 @@ def main():
     for fn in (front, middle, back):      # eager warm-up (module load, attributes)
         fn()
     torch.cuda.synchronize()
-    if args.no_graph:
+    if args.no_graph or collective == "p2p":     # symmetric-memory barriers run eagerly
         run = (front, middle, back)
     else:                                  # one CUDA graph per phase; events between replays
         run = tuple(path.capture(fn).replay for fn in (front, middle, back))
@@ -467,10 +490,7 @@ def main():
             path.segment()
             path.candidates(w.tau_s)
             if args.mode == "headshard":
-                path.distance_call(w.tau_b, L.DIST_PARTIAL)
-                if world > 1:
-                    dist.all_reduce(path.partial_sq[:counts["pairs"] * sh.num_layers * 2])
-                path.distance_call(w.tau_b, L.DIST_FINALIZE)
+                headshard_distance()
             else:
                 path.distance_call(w.tau_b)
             path.remap()
@@ -481,7 +501,7 @@ def main():
             out_cnt.copy_(cnt_dev, non_blocking=True)
 
         e2e_body = e2e_step
-        e2e_graph = not args.no_graph and args.mode == "seq"
+        e2e_graph = not args.no_graph and collective == "none"
         if e2e_graph:
             # a serving loop replays the round as one CUDA graph: memcpy nodes read the pinned
             # host inputs / write the pinned host outputs at replay time, the ABI calls in between
@@ -544,7 +564,10 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak" if args.mode == "seq" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": describe(args.config, w, world, args.mode),
+        "config": {**describe(args.config, w, world, args.mode),
+                   **({"collective": {"p2p": "FINALIZE reads all ranks' partial sums over NVLink (symmetric memory)",
+                                      "nccl": "NCCL all-reduce of partial sums, then FINALIZE"}[collective]}
+                      if collective != "none" else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "distance_kernel (memshare_block_distance)",
                      "kernel_ms": d_ms, "kernel_share_of_step": d_ms / ms_step, "algorithmic_bytes": alg_bytes,

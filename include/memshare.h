@@ -269,6 +269,23 @@ const char* memshare_status_string(memshare_status status);
 /* MEMSHARE_ABI_VERSION of the loaded library. */
 int32_t memshare_abi_version(void);
 
+/* memshare_block_distance_finalize_peers -- FINALIZE for the KV-head-sharded mode with the
+ * cross-rank reduction fused in (reading R17): instead of an all-reduce of the
+ * PARTIAL squared sums followed by FINALIZE, each rank's finalisation loads every rank's
+ * partial_sq directly over NVLink / NVSwitch (peer mappings, e.g. symmetric memory) and sums them
+ * in rank order, so every rank computes bit-identical distances and decisions.
+ *   partial_peers  DEVICE array [num_peers] of device pointers, valid on the calling GPU: rank r's
+ *                  float [pair_cap][N][2] PARTIAL output (rank order, 1 <= num_peers <= 64); every
+ *                  rank's PARTIAL call must be complete and visible before this call runs (the
+ *                  caller issues a device-side barrier, e.g. symmetric-memory barrier, first)
+ *   dims           num_kv_heads_global is the h of the 2dh normaliser
+ *   other arguments and outputs as memshare_block_distance in FINALIZE mode. */
+memshare_status memshare_block_distance_finalize_peers(
+    const float* const* partial_peers, int32_t num_peers, const memshare_dims* dims_host,
+    const memshare_block_pair* pairs, const int64_t* target_off, const int64_t* num_pairs,
+    const int64_t* num_targets, int64_t pair_cap, int64_t target_cap, float tau_b, float* distance, uint8_t* under,
+    memshare_decision* decisions, void* workspace, size_t workspace_bytes, int32_t* device_status, void* stream);
+
 /* ---------------------------------------------------------------------------------------- f1
  * Decode-loop integration: the steps on either side of the MemShare path. Shared blocks are
  * read "through the block table" by paged attention, with no copy.

@@ -64,6 +64,8 @@ def _load():
     L.memshare_block_distance.restype = I32
     L.memshare_block_distance_workspace_size.argtypes = [P, I32, I64, I64, I32]
     L.memshare_block_distance_workspace_size.restype = U64
+    L.memshare_block_distance_finalize_peers.argtypes = [P, I32, P, P, P, P, P, I64, I64, F32, P, P, P, P, U64, P, P]
+    L.memshare_block_distance_finalize_peers.restype = I32
     L.memshare_remap.argtypes = [P, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, P, U64, P, P]
     L.memshare_remap.restype = I32
     L.memshare_remap_workspace_size.argtypes = [I32, I64]
@@ -168,6 +170,17 @@ def block_distance(pool: KVPool | None, dims: Dims, pairs, target_off, num_pairs
         _ptr(distance), _ptr(under), _ptr(decisions), _ptr(workspace),
         0 if workspace is None else workspace.numel() * workspace.element_size(), _ptr(device_status),
         _stream(stream))
+
+
+def block_distance_finalize_peers(peer_ptrs_dev, num_peers, dims: Dims, pairs, target_off, num_pairs, num_targets,
+                                  pair_cap, target_cap, tau_b, distance, under, decisions, workspace, device_status,
+                                  stream=None) -> int:
+    """peer_ptrs_dev: int64 CUDA tensor [num_peers] of device pointers (every rank's partial_sq)."""
+    return lib.memshare_block_distance_finalize_peers(
+        _ptr(peer_ptrs_dev), num_peers, ctypes.byref(dims), _ptr(pairs), _ptr(target_off), _ptr(num_pairs),
+        _ptr(num_targets), pair_cap, target_cap, float(tau_b), _ptr(distance), _ptr(under), _ptr(decisions),
+        _ptr(workspace), 0 if workspace is None else workspace.numel() * workspace.element_size(),
+        _ptr(device_status), _stream(stream))
 
 
 # -------------------------------------------------------------------------------------- a7

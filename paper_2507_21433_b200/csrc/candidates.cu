@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
 #pragma unroll 4
         for (int32_t i = threadIdx.x; i < chi - clo; i += kNT1) sm.tok[i] = __ldg(t + clo + i);
         __syncthreads();
+        if (jb == 0 && clo == lo) DBG_T(14);
         if (!(a.dbg_skip & 1)) {
           if (tb.global)
             stream_history<true>(tb.slots, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,

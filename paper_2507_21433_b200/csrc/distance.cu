@@ -145,6 +145,8 @@ struct DistArgs {
   int32_t mode;
   int32_t metric;        // MEMSHARE_METRIC_EUCLIDEAN | MEMSHARE_METRIC_COSINE
   float* partial_sq;
+  const float* const* peers;  // FINALIZE over peer memory: every rank's partial_sq, rank order
+  int32_t num_peers;
   float tau_b;
   float* distance;
   uint8_t* under;
@@ -236,7 +238,15 @@ __device__ __forceinline__ float sum_warps(const DistArgs& a, const float* buf, 
 }
 
 __device__ __forceinline__ float sum_part(const DistArgs& a, int64_t p, int32_t l, int32_t kv, bool from_partial) {
-  if (from_partial) return __ldcg(a.partial_sq + ((p * a.N + l) * 2 + kv));
+  if (from_partial) {
+    const int64_t o = (p * a.N + l) * 2 + kv;
+    if (a.num_peers == 0) return __ldcg(a.partial_sq + o);
+    // the cross-rank reduction fused into finalisation: one load per rank over NVLink (peer
+    // mappings of the ranks' partial_sq), summed in rank order -> identical on every rank
+    float s = __ldcv(a.peers[0] + o);
+    for (int r = 1; r < a.num_peers; ++r) s += __ldcv(a.peers[r] + o);
+    return s;
+  }
   return sum_warps(a, a.ws.wpart, p, l, kv);
 }
 
@@ -1097,3 +1107,39 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 0);
   return launch_status();
 }
+
+extern "C" memshare_status memshare_block_distance_finalize_peers(
+    const float* const* partial_peers, int32_t num_peers, const memshare_dims* dims,
+    const memshare_block_pair* pairs, const int64_t* target_off, const int64_t* num_pairs,
+    const int64_t* num_targets, int64_t pair_cap, int64_t target_cap, float tau_b, float* distance, uint8_t* under,
+    memshare_decision* decisions, void* workspace, size_t workspace_bytes, int32_t* device_status, void* stream) {
+  if (!partial_peers || num_peers < 1 || num_peers > 64 || !dims || !pairs || !target_off || !num_pairs ||
+      !num_targets || !distance || !under || !decisions || !workspace || !device_status)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (pair_cap < 0 || pair_cap > ((int64_t)1 << 30) || target_cap < 0 || target_cap > (int64_t)INT32_MAX)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  const memshare_dims dm = *dims;
+  if (dm.num_layers < 1 || dm.num_layers > 256 || dm.num_kv_heads_global < 1 || dm.block_size < 1 ||
+      dm.head_dim < 8 || dm.head_dim % 8 != 0)
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (!(tau_b >= 0.f)) return MEMSHARE_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < memshare_block_distance_workspace_size(dims, 0, pair_cap, target_cap, MEMSHARE_METRIC_EUCLIDEAN))
+    return MEMSHARE_ERR_INVALID_ARGUMENT;
+  DistArgs a{};
+  a.N = dm.num_layers; a.d = dm.block_size; a.h_global = dm.num_kv_heads_global;
+  const int64_t slice_bytes = (int64_t)dm.block_size * dm.num_kv_heads_local * dm.head_dim * 2;
+  a.slice_bytes = (int32_t)slice_bytes;
+  a.n_sub = n_sub_of(slice_bytes);
+  a.pairs = pairs; a.target_off = target_off; a.num_pairs = num_pairs; a.num_targets = num_targets;
+  a.pair_cap = pair_cap; a.target_cap = target_cap; a.mode = MEMSHARE_DIST_FINALIZE;
+  a.metric = MEMSHARE_METRIC_EUCLIDEAN; a.tau_b = tau_b;
+  a.distance = distance; a.under = under; a.decisions = decisions; a.status = device_status;
+  a.peers = partial_peers; a.num_peers = num_peers;
+  Ws w{static_cast<char*>(workspace), 0};
+  a.ws = dist_layout(w, a.N, a.n_sub, 0, pair_cap, target_cap, MEMSHARE_METRIC_EUCLIDEAN);
+  const int64_t tc = target_cap < 1 ? 1 : target_cap;
+  const int fin_grid = (int)(tc < 8 * sm_count() ? tc : 8 * sm_count());
+  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, static_cast<cudaStream_t>(stream), a, 1);
+  return launch_status();
+}
+

@@ -148,6 +148,13 @@ class MemSharePath:
                                  mode, ps, tau_b, self.distance, self.under, self.decisions, self.workspace,
                                  self.status, self.stream, metric), "block_distance")
 
+    def finalize_peers(self, tau_b, peer_ptrs_dev, num_peers):
+        """KV-head-sharded FINALIZE reading every rank's partial_sq over peer memory (rank order)."""
+        L.check(L.block_distance_finalize_peers(peer_ptrs_dev, num_peers, self.dims, self.pairs, self.target_off,
+                                                self.num_pairs, self.num_targets, self.caps.pair, self.caps.target,
+                                                tau_b, self.distance, self.under, self.decisions, self.workspace,
+                                                self.status, self.stream), "block_distance_finalize_peers")
+
     def remap(self):
         L.check(L.remap(self.table, self.table_stride, self.num_seqs, self.refcount, self.num_blocks, self.free_list,
                         self.free_count, self.decisions, self.num_targets, self.caps.target, self.block_size,

@@ -44,10 +44,10 @@ for r in range(cs):
     rr = (t[owner + r] - t0) / 1e3
     print(f"rank {r}: start {rr[0]:.2f} table {rr[1]:.2f} staged {rr[10]:.2f} loop-end {rr[7]:.2f}")
 r = (t[owner] - t0) / 1e3
-names = {0: "start", 1: "table", 10: "hist staged", 11: "stream done", 2: "select", 3: "sort", 4: "stash",
+names = {0: "start", 1: "table", 10: "hist staged", 14: "tokens staged", 11: "stream done", 2: "select", 3: "sort", 4: "stash",
          5: "prepare", 6: "count", 7: "loop end"}
 print("steps", G, "owner CTA", owner)
-for k in (0, 1, 10, 11, 2, 3, 4, 5, 6, 7):
+for k in (0, 1, 10, 14, 11, 2, 3, 4, 5, 6, 7):
     print(f"  {names[k]:12s} {r[k]:7.2f} us")
 cyc = t[owner, 13] - t[owner, 12]
 ns = t[owner, 11] - t[owner, 10]

@@ -72,6 +72,14 @@ def test_invalid_arguments_rejected_before_any_launch(lib):
     assert L.memshare_block_distance(nul, ctypes.byref(dims), nul, nul, nul, nul, 0, 0, 0, 0, nul, 0.1, nul, nul,
                                      nul, nul, 0, nul, nul) == 1
     assert L.memshare_remap(nul, 0, 0, nul, 0, nul, nul, nul, nul, 0, 16, nul, nul, nul, 0, nul, nul) == 1
+    good = lib.Dims(64, 1, 8, 128, 16)
+    buf = (ctypes.c_char * 64)()
+    # finalize over peers: no peers / too many peers / null outputs -> INVALID_ARGUMENT
+    for npeers in (0, 65):
+        assert L.memshare_block_distance_finalize_peers(buf, npeers, ctypes.byref(good), buf, buf, buf, buf, 1, 1,
+                                                        0.1, buf, buf, buf, buf, 64, buf, nul) == 1
+    assert L.memshare_block_distance_finalize_peers(buf, 2, ctypes.byref(good), buf, buf, buf, buf, 1, 1, 0.1, nul,
+                                                    buf, buf, buf, 64, buf, nul) == 1
 
 
 def test_f1_host_checks_and_admission(lib):

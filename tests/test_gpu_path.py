@@ -220,8 +220,9 @@ def test_distance_properties_on_gpu():
 def test_head_sharded_two_shards_on_one_gpu():
     """KV-head sharding (bench.py --mode headshard) with both shards on this
     GPU: each shard holds 4 of the 8 KV heads, runs a1-a4 (identical pair lists) and PARTIAL;
-    the device-side sum of the partial squared sums stands in for the NCCL all-reduce; FINALIZE
-    with the global h must match the fp64 oracle on the full 8-head pool."""
+    memshare_block_distance_finalize_peers reads both partials through a pointer array (the fused
+    peer-memory reduction) and must equal, bit for bit, the device-side sum + FINALIZE (the NCCL
+    all-reduce stand-in); both must match the fp64 oracle on the full 8-head pool."""
     import torch
     from paper_2507_21433_b200 import _lib as L
     shape = kv.KVShape(4, 8, 128, 16)
@@ -238,11 +239,21 @@ def test_head_sharded_two_shards_on_one_gpu():
     for k_ in c0["pairs"]:
         assert np.array_equal(c0["pairs"][k_], c1["pairs"][k_]), k_
     p = shards[0]
+    # fused reduction: FINALIZE loads both shards' partial sums through a device pointer array
+    # (on a multi-GPU node these are symmetric-memory peer mappings over NVLink)
+    ptrs = torch.tensor([q.partial_sq.data_ptr() for q in shards], dtype=torch.int64, device="cuda")
+    p.finalize_peers(w.tau_b, ptrs, 2)
+    torch.cuda.synchronize()
+    assert p.read_status() == 0
+    gp = p.read_distance()
     p.partial_sq += shards[1].partial_sq                   # the all-reduce (sum over head shards)
     p.distance_call(w.tau_b, L.DIST_FINALIZE)
     torch.cuda.synchronize()
     assert p.read_status() == 0 and shards[1].read_status() == 0
     gd = p.read_distance()
+    assert np.array_equal(gp["distance"], gd["distance"])   # same rank-order fp32 sum -> bit-identical
+    for k_ in gd["decisions"]:
+        assert np.array_equal(gp["decisions"][k_], gd["decisions"][k_]), k_
     pr = c0["pairs"]
     kh, vh, ls, bs = w.host_pool()
     D = oracle.block_distance(kh, vh, ls, bs, shape.num_layers, shape.num_kv_heads, shape.num_kv_heads,
