@@ -18,7 +18,7 @@ namespace {
 constexpr int kNT = 1024;
 
 struct RemapWs {
-  int32_t* last_dec;   // [num_blocks], -1
+  int32_t* last_dec;   // [num_blocks]; entries of blocks a call decrements are reset to -1 first
   int32_t* old_of;     // [target_cap]
 };
 
@@ -65,6 +65,12 @@ __global__ void __launch_bounds__(kNT) remap_kernel(int32_t* __restrict__ table,
   }
   __syncthreads();
   if (bad) return;
+  // reset the last-decrement slot of every block this call may decrement (no O(num_blocks) memset)
+  for (int64_t i = threadIdx.x; i < T; i += kNT) {
+    const memshare_decision d = dec[i];
+    if (d.accepted) ws.last_dec[table[(int64_t)d.seq * table_stride + d.target_logical]] = -1;
+  }
+  __syncthreads();
   // phase 1: apply in parallel (distinct targets -> distinct table entries)
   int64_t aff = 0;
   for (int64_t i = threadIdx.x; i < T; i += kNT) {
@@ -144,8 +150,6 @@ extern "C" memshare_status memshare_remap(int32_t* block_table, int32_t table_st
   Ws w{static_cast<char*>(workspace), 0};
   RemapWs ws = remap_layout(w, num_blocks, target_cap);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(ws.last_dec, 0xFF, sizeof(int32_t) * ((size_t)num_blocks + 1), st) != cudaSuccess)
-    return MEMSHARE_ERR_CUDA;
   launch_pdl(remap_kernel, dim3(1), dim3(kNT), 0, st, block_table, table_stride, num_seqs, refcount, num_blocks, free_list, free_count,
                                   decisions, num_targets, target_cap, block_size, num_freed, affected_tokens, ws,
                                   device_status);
