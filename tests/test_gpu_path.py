@@ -89,6 +89,28 @@ def test_stage1_and_pair_variants(tau_s, top_k, pairing):
     full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing)
 
 
+@pytest.mark.parametrize("seed", range(24))
+def test_randomized_configurations(seed):
+    """Seeded fuzz over the parameter space: KV shapes (incl. 10 heads, block sizes 8 / 32),
+    pairing, tau_s, top_k and call granularity, each through the full parity check."""
+    rng = np.random.default_rng(1000 + seed)
+    shape = [kv.KVShape(2, 2, 64, 16), kv.KVShape(3, 10, 128, 16), kv.KVShape(4, 8, 128, 8),
+             kv.KVShape(2, 4, 64, 32)][seed % 4]
+    num_seqs = int(rng.integers(1, 4))
+    length = int(rng.integers(700, 2600))
+    w = workloads.small(shape, num_seqs, length, seed=seed, gen_start=int(rng.integers(0, 200)))
+    pairing = [oracle.ALIGNED, oracle.CROSS][int(rng.integers(0, 2))]
+    tau_s = float(rng.choice([0.3, 0.6, 0.8, 0.95]))
+    top_k = int(rng.choice([0, 0, 1, 3]))
+    mode = int(rng.integers(0, 3))
+    if mode == 2:
+        cb = [int(x) for x in rng.integers(0, 6, num_seqs)]
+        ce = [b + int(x) for b, x in zip(cb, rng.integers(1, 12, num_seqs))]
+        full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=oracle.CUR_RANGE, cb=cb, ce=ce)
+    else:
+        full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=[oracle.CUR_ALL, oracle.CUR_LAST][mode])
+
+
 def test_online_modes():
     """LAST with 3 sequences runs Stage 1 as 8-CTA clusters per current step (DSMEM sum of the
     ranks' partial dots); RANGE runs one CTA per step."""
