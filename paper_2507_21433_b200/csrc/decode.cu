@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(kAppNT) append_alloc_kernel(int32_t* table, in
                                                               int32_t* refcount, int32_t num_blocks,
                                                               const int32_t* free_list, int64_t* free_count,
                                                               int32_t block_size, AppWs ws, int32_t* status) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int64_t sh[kAppNT / 32 + 1];
   const int64_t fc = *free_count;
   int err = 0;          // 2 capacity, 3 corruption, 1 invalid
@@ -116,6 +118,8 @@ __global__ void __launch_bounds__(256) append_copy_kernel(uint16_t* k, uint16_t*
                                                           int64_t block_stride, int32_t num_layers, int32_t num_seqs,
                                                           int32_t row_elems, const uint16_t* new_k,
                                                           const uint16_t* new_v, AppWs ws) {
+  pdl_trigger();
+  pdl_wait();
   if (__ldcg(ws.ok) == 0) return;
   const int lane = threadIdx.x & 31;
   const int32_t vec = row_elems / 8;             // 16-byte vectors per row
@@ -210,6 +214,8 @@ __device__ __forceinline__ float bf16_hi(uint32_t x) { return __uint_as_float(x 
 // with an fp32 online softmax in between (row statistics per query head).
 template <int DH>
 __global__ void __launch_bounds__(kAttNT) attn_split_kernel(AttArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int KS = DH / 16;                 // k-steps of Q K^T
   constexpr int MT = DH / 16;                 // m-tiles (16 dims) of O^T
   constexpr int CH = DH / 8;                  // 16-byte chunks per row
@@ -381,6 +387,8 @@ constexpr size_t attn_smem_bytes() {
 // One warp per (sequence, query head): combine the chunk partials.
 template <int DH>
 __global__ void attn_combine_kernel(AttArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int VPL = DH / 32;
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -444,12 +452,12 @@ extern "C" memshare_status memshare_kv_append(void* k_pool, void* v_pool, int64_
   Ws w{static_cast<char*>(workspace), 0};
   const AppWs ws = app_layout(w, num_seqs);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  append_alloc_kernel<<<1, kAppNT, 0, st>>>(block_table, table_stride, num_seqs, seq_len, active, refcount, num_blocks,
+  launch_pdl(append_alloc_kernel, dim3(1), dim3(kAppNT), 0, st, block_table, table_stride, num_seqs, seq_len, active, refcount, num_blocks,
                                             free_list, free_count, d.block_size, ws, device_status);
   const int64_t rows = (int64_t)d.num_layers * num_seqs;
   if (rows > INT32_MAX) return MEMSHARE_ERR_INVALID_ARGUMENT;
   const int grid = (int)std::min<int64_t>((rows + 7) / 8, 8 * sm_count());    // 8 warps (rows) per CTA
-  append_copy_kernel<<<grid, 256, 0, st>>>(static_cast<uint16_t*>(k_pool), static_cast<uint16_t*>(v_pool),
+  launch_pdl(append_copy_kernel, dim3(grid), dim3(256), 0, st, static_cast<uint16_t*>(k_pool), static_cast<uint16_t*>(v_pool),
                                            layer_stride, block_stride, d.num_layers, num_seqs, (int32_t)row,
                                            static_cast<const uint16_t*>(new_k), static_cast<const uint16_t*>(new_v),
                                            ws);
@@ -528,11 +536,11 @@ extern "C" memshare_status memshare_paged_attention_decode(
   const int64_t warps = (int64_t)num_seqs * num_q_heads;
   const int cgrid = (int)((warps * 32 + 255) / 256);
   if (d.head_dim == 128) {
-    attn_split_kernel<128><<<grid, kAttNT, attn_smem_bytes<128>(), st>>>(a);
-    attn_combine_kernel<128><<<cgrid, 256, 0, st>>>(a);
+    launch_pdl(attn_split_kernel<128>, grid, dim3(kAttNT), attn_smem_bytes<128>(), st, a);
+    launch_pdl(attn_combine_kernel<128>, dim3(cgrid), dim3(256), 0, st, a);
   } else {
-    attn_split_kernel<64><<<grid, kAttNT, attn_smem_bytes<64>(), st>>>(a);
-    attn_combine_kernel<64><<<cgrid, 256, 0, st>>>(a);
+    launch_pdl(attn_split_kernel<64>, grid, dim3(kAttNT), attn_smem_bytes<64>(), st, a);
+    launch_pdl(attn_combine_kernel<64>, dim3(cgrid), dim3(256), 0, st, a);
   }
   return launch_status();
 }

@@ -54,10 +54,12 @@ def EP(sh):
 
 
 def flush_l2():
+    """Evict L2 by READING a 512 MB buffer (a write-based flush would leave ~126 MB of dirty lines
+    whose write-back then competes with the timed kernel's reads)."""
     global FLUSH
     if FLUSH is None:
-        FLUSH = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    FLUSH.zero_()
+        FLUSH = torch.ones(64 << 20, dtype=torch.int64, device="cuda")
+    FLUSH.sum()
 
 
 def time_us(fn, reps=30, flush=False, warm=3):
