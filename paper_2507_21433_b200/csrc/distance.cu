@@ -54,6 +54,9 @@ namespace {
 #ifndef MS_PIPE
 #define MS_PIPE 1                 // 1: software-pipelined single-target Euclidean consumers
 #endif
+#ifndef MS_ST_MAXKRE
+#define MS_ST_MAXKRE 10           // largest single-target stage, in 4 KiB units (10 = 40 KiB)
+#endif
 #ifndef MS_SUB_UNPACK
 #define MS_SUB_UNPACK 0           // 1: t - s via ALU unpack + FFMA2 instead of FHFMA.BF16
 #endif
@@ -977,6 +980,232 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
   }
 }
 
+// ------------------------------------------------- single-target kernel, stage size per shape
+// The shipped Euclidean path. Template parameter KRE = 16-byte chunks per consumer thread per
+// stage, so a stage is KRE * 4 KiB and holds one (layer, K|V) slice or an equal part of it
+// (32B shape: 32 KiB slices -> KRE 8, one stage per slice; Phi-4: 40 KiB -> two 20 KiB stages,
+// KRE 5; tiny: 4 KiB -> KRE 1). The ring keeps the same ~192 KiB of shared memory, so smaller
+// stages mean MORE stages in flight: the ring turns over once per TMA round trip, so the stage
+// rate, not the byte rate, is what a fixed-size ring of small stages would limit.
+constexpr int kChunkUnit = 16 * kConsumers;                 // 4 KiB: one chunk per consumer thread
+constexpr int kRingBytes = 200 * 1024;                    // shared-memory ring of the single-target kernel
+constexpr int kMaxKre = 10;                                // largest stage: 40 KiB (one Phi-4 slice)
+constexpr int kMaxRingStages = 48;
+
+template <int KRE>
+struct StCfg {
+  static constexpr int kStageB = KRE * kChunkUnit;
+  static constexpr int kNSt = (kRingBytes / kStageB) < kMaxRingStages ? kRingBytes / kStageB : kMaxRingStages;
+};
+
+template <int KRE>
+struct StSmem {
+  alignas(128) uint8_t ring[StCfg<KRE>::kNSt][StCfg<KRE>::kStageB];
+  alignas(16) int4 hdr[StCfg<KRE>::kNSt];
+  alignas(8) uint64_t full[StCfg<KRE>::kNSt];
+  uint64_t empty[StCfg<KRE>::kNSt];
+};
+
+template <int KRE>
+__device__ __forceinline__ void st_producer(StSmem<KRE>& sm, const DistArgs& a, int lane) {
+  constexpr int NS = StCfg<KRE>::kNSt;
+  const int64_t I = clamp_count(a.num_targets, a.target_cap);
+  const int64_t Pn = clamp_count(a.num_pairs, a.pair_cap);
+  const int64_t total = I * a.n_chunks;
+  int stage = 0;
+  uint32_t ph = 0;
+  // one unit = (target, chunk of lpi layers); the next unit's ids are loaded one unit ahead
+  struct UnitMeta { int64_t lc, t; int32_t lo, np, tphys, sp0, sp1; };
+  auto load_meta = [&](int64_t u) {
+    UnitMeta m{0, 0, 0, 0, 0, 0, 0};
+    if (u >= total) return m;
+    m.lc = u / I;
+    m.t = u - m.lc * I;
+    const int64_t lo = __ldcg(a.target_off + m.t);
+    int64_t hi = __ldcg(a.target_off + m.t + 1);
+    if (hi > Pn) hi = Pn;
+    m.lo = (int32_t)lo;
+    m.np = (int32_t)(hi > lo ? hi - lo : 0);
+    if (m.np > 0) m.tphys = a.pairs[lo].target_phys;
+    if (lane < m.np) m.sp0 = a.pairs[lo + lane].source_phys;
+    if (lane + 32 < m.np) m.sp1 = a.pairs[lo + 32 + lane].source_phys;
+    return m;
+  };
+  int64_t unit = 0, next = 0;
+  if (lane == 0) {
+    unit = (int64_t)atomicAdd(a.ws.ticket, 1u);
+    next = (int64_t)atomicAdd(a.ws.ticket, 1u);
+  }
+  unit = __shfl_sync(0xffffffffu, unit, 0);
+  next = __shfl_sync(0xffffffffu, next, 0);
+  UnitMeta cur = load_meta(unit);
+  while (unit < total) {
+    int64_t next2 = 0;
+    if (lane == 0) next2 = (int64_t)atomicAdd(a.ws.ticket, 1u);
+    const UnitMeta nm = load_meta(next);
+    if (cur.np > 0) {
+      const int32_t tphys = checked_phys(a, cur.tphys);
+      const int32_t l0 = (int32_t)cur.lc * a.lpi;
+      const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
+      for (int32_t c0 = 0; c0 < cur.np; c0 += 64) {
+        const int32_t cn = (cur.np - c0) < 64 ? cur.np - c0 : 64;
+        int32_t sa = cur.sp0, sb = cur.sp1;
+        if (c0 > 0) {
+          sa = (lane < cn) ? a.pairs[cur.lo + c0 + lane].source_phys : 0;
+          sb = (lane + 32 < cn) ? a.pairs[cur.lo + c0 + 32 + lane].source_phys : 0;
+        }
+        for (int32_t l = l0; l < l1; ++l)
+          for (int32_t kv = 0; kv < 2; ++kv) {
+            const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
+            for (int32_t sub = 0; sub < a.n_sub; ++sub) {
+              const int32_t boff = sub * StCfg<KRE>::kStageB;
+              for (int32_t q = -1; q < cn; ++q) {                 // q = -1: the target
+                const int32_t v = __shfl_sync(0xffffffffu, (q & 32) ? sb : sa, q < 0 ? 0 : (q & 31));
+                if (lane == 0) {
+                  const int32_t phys = q < 0 ? tphys : checked_phys(a, v);
+                  const int64_t po = q < 0 ? 0 : (int64_t)(cur.lo + c0 + q);
+                  mbar_wait(&sm.empty[stage], ph ^ 1u);
+                  sm.hdr[stage] = make_hdr((((po * a.N + l) * 2 + kv) * a.n_sub + sub) * kConsumerWarps,
+                                           StCfg<KRE>::kStageB, q < 0 ? H_ANCHOR : H_PAIR);
+                  mbar_expect_tx(&sm.full[stage], (uint32_t)StCfg<KRE>::kStageB);
+                  bulk_g2s(sm.ring[stage], base + (int64_t)phys * a.block_stride_b + boff,
+                           (uint32_t)StCfg<KRE>::kStageB, &sm.full[stage]);
+                  if (++stage == NS) { stage = 0; ph ^= 1u; }
+                }
+              }
+            }
+          }
+      }
+    }
+    __syncwarp();
+    unit = next;
+    next = __shfl_sync(0xffffffffu, next2, 0);
+    cur = nm;
+  }
+  stage = __shfl_sync(0xffffffffu, stage, 0);
+  ph = __shfl_sync(0xffffffffu, ph, 0);
+  if (lane == 0) {
+    mbar_wait(&sm.empty[stage], ph ^ 1u);
+    sm.hdr[stage] = make_hdr(0, 0, H_STOP);
+    mbar_arrive(&sm.full[stage]);
+  }
+}
+
+template <int KRE>
+__device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (&x)[KRE], float2 (&T)[KRE * 4],
+                                        int warp, int lane) {
+  if (h.w & H_ANCHOR) {
+#pragma unroll
+    for (int r = 0; r < KRE; ++r) {
+      T[4 * r + 0] = bf2_to_f2(x[r].x);
+      T[4 * r + 1] = bf2_to_f2(x[r].y);
+      T[4 * r + 2] = bf2_to_f2(x[r].z);
+      T[4 * r + 3] = bf2_to_f2(x[r].w);
+    }
+  } else if (h.w & H_PAIR) {
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < KRE; ++r) {
+      const float2 d0 = sub_bf2(x[r].x, T[4 * r + 0]);
+      const float2 d1 = sub_bf2(x[r].y, T[4 * r + 1]);
+      const float2 d2 = sub_bf2(x[r].z, T[4 * r + 2]);
+      const float2 d3 = sub_bf2(x[r].w, T[4 * r + 3]);
+      acc0 = __ffma2_rn(d0, d0, acc0);
+      acc1 = __ffma2_rn(d1, d1, acc1);
+      acc0 = __ffma2_rn(d2, d2, acc0);
+      acc1 = __ffma2_rn(d3, d3, acc1);
+    }
+    const float s = warp_sum((acc0.x + acc0.y) + (acc1.x + acc1.y));
+    if (lane == 0) a.ws.wpart[(int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp] = s;
+  }
+}
+
+template <int KRE>
+__global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
+  constexpr int NS = StCfg<KRE>::kNSt;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StSmem<KRE>& sm = *reinterpret_cast<StSmem<KRE>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  if (warp == kConsumerWarps) {
+    st_producer<KRE>(sm, a, lane);
+    return;
+  }
+  // consumers: ping-pong register buffers (the next stage is copied while this one is evaluated)
+  float2 T[KRE * 4];
+  uint4 xa[KRE], xb[KRE];
+  int stage = 0;
+  uint32_t ph = 0;
+  auto load = [&](uint4 (&dst)[KRE]) {
+    const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
+#pragma unroll
+    for (int r = 0; r < KRE; ++r) dst[r] = src[tid + r * kConsumers];
+  };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (++stage == NS) { stage = 0; ph ^= 1u; }
+  };
+  mbar_wait(&sm.full[stage], ph);
+  int4 ha = sm.hdr[stage], hb;
+  if (ha.w & H_STOP) return;
+  load(xa);
+  release();
+  for (;;) {
+    mbar_wait(&sm.full[stage], ph);
+    hb = sm.hdr[stage];
+    if (!(hb.w & H_STOP)) load(xb);
+    st_eval<KRE>(a, ha, xa, T, warp, lane);
+    if (hb.w & H_STOP) break;
+    release();
+    mbar_wait(&sm.full[stage], ph);
+    ha = sm.hdr[stage];
+    if (!(ha.w & H_STOP)) load(xa);
+    st_eval<KRE>(a, hb, xb, T, warp, lane);
+    if (ha.w & H_STOP) break;
+    release();
+  }
+}
+
+template <int KRE>
+static cudaError_t launch_st(const DistArgs& a, cudaStream_t st) {
+  static bool attr_set_dev[kMaxDevices] = {};
+  bool& attr_set = attr_set_dev[current_device()];
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(distance_st_kernel<KRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(StSmem<KRE>));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  return launch_pdl(distance_st_kernel<KRE>, dim3(sm_count()), dim3(kThreads), sizeof(StSmem<KRE>), st, a);
+}
+
+static cudaError_t launch_st_any(int kre, const DistArgs& a, cudaStream_t st) {
+  switch (kre) {
+    case 1: return launch_st<1>(a, st);
+    case 2: return launch_st<2>(a, st);
+    case 3: return launch_st<3>(a, st);
+    case 4: return launch_st<4>(a, st);
+    case 5: return launch_st<5>(a, st);
+    case 6: return launch_st<6>(a, st);
+    case 7: return launch_st<7>(a, st);
+    case 8: return launch_st<8>(a, st);
+    case 9: return launch_st<9>(a, st);
+    case 10: return launch_st<10>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // Finalisation: one CTA per target (grid-stride). FULL/PARTIAL read the per-warp partials the
 // streaming kernel left in the workspace (kernel boundary = the only synchronisation needed);
 // FINALIZE reads partial squared sums already reduced across ranks.
@@ -995,8 +1224,41 @@ __global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int fr
 
 using namespace ms;
 
+// host: stage geometry of the single-target kernel for this slice size -- KRE (16-byte chunks per
+// consumer thread, stage = KRE * 4 KiB) and the number of equal sub-slices; KRE = 0 when the slice
+// is not a multiple of 4 KiB that splits evenly (then the generic kernel runs).
+// MEMSHARE_ST_MAXKRE (1..10, tuning) caps KRE, i.e. forces smaller stages and a deeper ring.
+static int st_maxk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MEMSHARE_ST_MAXKRE");
+    v = e ? atoi(e) : MS_ST_MAXKRE;
+    if (v < 1 || v > kMaxKre) v = kMaxKre;
+  }
+  return v;
+}
+
+static int st_kre(int64_t slice_bytes, int32_t* n_sub) {
+  if (slice_bytes <= 0 || slice_bytes % kChunkUnit != 0) return 0;
+  const int64_t units = slice_bytes / kChunkUnit;
+  const int maxk = st_maxk();
+  for (int64_t ns = (units + maxk - 1) / maxk; ns <= units; ++ns)
+    if (units % ns == 0) {
+      if (n_sub) *n_sub = (int32_t)ns;
+      return (int)(units / ns);
+    }
+  return 0;
+}
+
 static int32_t n_sub_of(int64_t slice_bytes) {
   return (int32_t)((slice_bytes + kStageBytes - 1) / kStageBytes);
+}
+
+// workspace: room for either kernel's sub-slice count
+static int32_t n_sub_ws(int64_t slice_bytes) {
+  int32_t ns = 0;
+  const int32_t g = n_sub_of(slice_bytes);
+  return (st_kre(slice_bytes, &ns) > 0 && ns > g) ? ns : g;
 }
 
 extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* dims, int32_t num_blocks,
@@ -1005,7 +1267,7 @@ extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* di
   if (metric != MEMSHARE_METRIC_EUCLIDEAN && metric != MEMSHARE_METRIC_COSINE) return 0;
   const int64_t slice = (int64_t)dims->block_size * dims->num_kv_heads_local * dims->head_dim * 2;
   Ws w{nullptr, 0};
-  dist_layout(w, dims->num_layers, n_sub_of(slice), num_blocks, pair_cap, target_cap, metric);
+  dist_layout(w, dims->num_layers, n_sub_ws(slice), num_blocks, pair_cap, target_cap, metric);
   return w.size();
 }
 
@@ -1057,6 +1319,13 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   a.slice_bytes = (int32_t)slice_bytes;
   a.n_sub = n_sub_of(slice_bytes);
   a.sub_bytes = (int32_t)(((slice_bytes / a.n_sub) + 15) / 16 * 16);
+  int32_t st_nsub = 0;
+  const int kre = (metric == MEMSHARE_METRIC_EUCLIDEAN && kAnchors == 1 && MS_PIPE && mode != MEMSHARE_DIST_FINALIZE)
+                      ? st_kre(slice_bytes, &st_nsub) : 0;
+  if (kre > 0) {                                      // equal sub-slices of exactly one stage each
+    a.n_sub = st_nsub;
+    a.sub_bytes = kre * kChunkUnit;
+  }
   static int lpi_env = -1;
   if (lpi_env < 0) {
     const char* e = getenv("MEMSHARE_LAYERS_PER_ITEM");
@@ -1100,7 +1369,9 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   int64_t plan_np2 = 1;
   while (plan_np2 < target_cap && plan_np2 < kPlanSortCap) plan_np2 <<= 1;
   if (kAnchors > 1) launch_pdl(plan_kernel, dim3(1), dim3(kPlanThreads), (size_t)plan_np2 * sizeof(unsigned long long), st, a);
-  if (metric == MEMSHARE_METRIC_COSINE)
+  if (kre > 0) {
+    if (launch_st_any(kre, a, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  } else if (metric == MEMSHARE_METRIC_COSINE)
     launch_pdl(distance_kernel<MEMSHARE_METRIC_COSINE>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
   else
     launch_pdl(distance_kernel<MEMSHARE_METRIC_EUCLIDEAN>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
