@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_kernel(DistArgs a) {
 // stages mean MORE stages in flight: the ring turns over once per TMA round trip, so the stage
 // rate, not the byte rate, is what a fixed-size ring of small stages would limit.
 constexpr int kChunkUnit = 16 * kConsumers;                 // 4 KiB: one chunk per consumer thread
-constexpr int kRingBytes = 200 * 1024;                    // shared-memory ring of the single-target kernel
+constexpr int kRingBytes = 224 * 1024;                    // shared-memory ring of the single-target kernel (of 227 KB)
 constexpr int kMaxKre = 10;                                // largest stage: 40 KiB (one Phi-4 slice)
 constexpr int kMaxRingStages = 48;
 
