@@ -555,9 +555,11 @@ def main():
     achieved = alg_bytes / (d_ms / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_distance_{args.config}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof):                   # the committed ncu capture of this exact workload
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            if int(pj.get("seqs_per_gpu", w.batch.num_seqs)) == w.batch.num_seqs and args.mode == "seq":
+                traffic = pj.get("dram_bytes_per_launch")
         except (ValueError, OSError):
             traffic = None
     line = {
