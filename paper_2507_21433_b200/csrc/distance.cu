@@ -1063,7 +1063,9 @@ __device__ __forceinline__ void st_producer(StSmem<KRE>& sm, const DistArgs& a, 
                 const int32_t v = __shfl_sync(0xffffffffu, (q & 32) ? sb : sa, q < 0 ? 0 : (q & 31));
                 if (lane == 0) {
                   const int32_t phys = q < 0 ? tphys : checked_phys(a, v);
-                  const int64_t po = q < 0 ? 0 : (int64_t)(cur.lo + c0 + q);
+                  // output row: the pair (Euclidean / cosine dot) or, for the target stage, the
+                  // target (cosine: its squared norm)
+                  const int64_t po = q < 0 ? cur.t : (int64_t)(cur.lo + c0 + q);
                   mbar_wait(&sm.empty[stage], ph ^ 1u);
                   sm.hdr[stage] = make_hdr((((po * a.N + l) * 2 + kv) * a.n_sub + sub) * kConsumerWarps,
                                            StCfg<KRE>::kStageB, q < 0 ? H_ANCHOR : H_PAIR);
@@ -1091,9 +1093,39 @@ __device__ __forceinline__ void st_producer(StSmem<KRE>& sm, const DistArgs& a, 
   }
 }
 
-template <int KRE>
+template <int KRE, int MET>
 __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (&x)[KRE], float2 (&T)[KRE * 4],
                                         int warp, int lane) {
+  if (MET == MEMSHARE_METRIC_COSINE) {
+    // f2 (reading R34): target stage -> cache + squared norm; source stage -> dot + squared norm
+    const int64_t o = (int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp;
+    float2 n0 = make_float2(0.f, 0.f), n1 = n0;
+    if (h.w & H_ANCHOR) {
+#pragma unroll
+      for (int r = 0; r < KRE; ++r) {
+        const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
+        T[4 * r + 0] = f0; T[4 * r + 1] = f1; T[4 * r + 2] = f2; T[4 * r + 3] = f3;
+        n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
+        n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
+      }
+      const float tn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
+      if (lane == 0) a.ws.wtn[o] = tn;
+    } else if (h.w & H_PAIR) {
+      float2 d0 = make_float2(0.f, 0.f), d1 = d0;
+#pragma unroll
+      for (int r = 0; r < KRE; ++r) {
+        const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
+        d0 = __ffma2_rn(T[4 * r + 0], f0, d0); d1 = __ffma2_rn(T[4 * r + 1], f1, d1);
+        d0 = __ffma2_rn(T[4 * r + 2], f2, d0); d1 = __ffma2_rn(T[4 * r + 3], f3, d1);
+        n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
+        n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
+      }
+      const float dot = warp_sum((d0.x + d0.y) + (d1.x + d1.y));
+      const float sn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
+      if (lane == 0) { a.ws.wpart[o] = dot; a.ws.wsn[o] = sn; }
+    }
+    return;
+  }
   if (h.w & H_ANCHOR) {
 #pragma unroll
     for (int r = 0; r < KRE; ++r) {
@@ -1120,7 +1152,7 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
   }
 }
 
-template <int KRE>
+template <int KRE, int MET>
 __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
   constexpr int NS = StCfg<KRE>::kNSt;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1165,43 +1197,58 @@ __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
     mbar_wait(&sm.full[stage], ph);
     hb = sm.hdr[stage];
     if (!(hb.w & H_STOP)) load(xb);
-    st_eval<KRE>(a, ha, xa, T, warp, lane);
+    st_eval<KRE, MET>(a, ha, xa, T, warp, lane);
     if (hb.w & H_STOP) break;
     release();
     mbar_wait(&sm.full[stage], ph);
     ha = sm.hdr[stage];
     if (!(ha.w & H_STOP)) load(xa);
-    st_eval<KRE>(a, hb, xb, T, warp, lane);
+    st_eval<KRE, MET>(a, hb, xb, T, warp, lane);
     if (ha.w & H_STOP) break;
     release();
   }
 }
 
-template <int KRE>
+template <int KRE, int MET>
 static cudaError_t launch_st(const DistArgs& a, cudaStream_t st) {
   static bool attr_set_dev[kMaxDevices] = {};
   bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(distance_st_kernel<KRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)sizeof(StSmem<KRE>));
+    const cudaError_t e = cudaFuncSetAttribute(distance_st_kernel<KRE, MET>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem<KRE>));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_pdl(distance_st_kernel<KRE>, dim3(sm_count()), dim3(kThreads), sizeof(StSmem<KRE>), st, a);
+  return launch_pdl(distance_st_kernel<KRE, MET>, dim3(sm_count()), dim3(kThreads), sizeof(StSmem<KRE>), st, a);
 }
 
-static cudaError_t launch_st_any(int kre, const DistArgs& a, cudaStream_t st) {
+// stage sizes with a single-target kernel: every KRE for the Euclidean metric; the cosine metric
+// for the shapes of the configs (tiny 4 KiB, 32B 32 KiB, Phi-4 40 KiB), others run the generic kernel
+static bool st_has(int kre, int metric) {
+  if (kre < 1 || kre > kMaxKre) return false;
+  return metric == MEMSHARE_METRIC_EUCLIDEAN || kre == 1 || kre == 8 || kre == 10;
+}
+
+static cudaError_t launch_st_any(int kre, int metric, const DistArgs& a, cudaStream_t st) {
+  if (metric == MEMSHARE_METRIC_COSINE) {
+    switch (kre) {
+      case 1: return launch_st<1, MEMSHARE_METRIC_COSINE>(a, st);
+      case 8: return launch_st<8, MEMSHARE_METRIC_COSINE>(a, st);
+      case 10: return launch_st<10, MEMSHARE_METRIC_COSINE>(a, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (kre) {
-    case 1: return launch_st<1>(a, st);
-    case 2: return launch_st<2>(a, st);
-    case 3: return launch_st<3>(a, st);
-    case 4: return launch_st<4>(a, st);
-    case 5: return launch_st<5>(a, st);
-    case 6: return launch_st<6>(a, st);
-    case 7: return launch_st<7>(a, st);
-    case 8: return launch_st<8>(a, st);
-    case 9: return launch_st<9>(a, st);
-    case 10: return launch_st<10>(a, st);
+    case 1: return launch_st<1, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 2: return launch_st<2, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 3: return launch_st<3, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 4: return launch_st<4, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 5: return launch_st<5, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 6: return launch_st<6, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 7: return launch_st<7, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 8: return launch_st<8, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 9: return launch_st<9, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
+    case 10: return launch_st<10, MEMSHARE_METRIC_EUCLIDEAN>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1320,8 +1367,8 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   a.n_sub = n_sub_of(slice_bytes);
   a.sub_bytes = (int32_t)(((slice_bytes / a.n_sub) + 15) / 16 * 16);
   int32_t st_nsub = 0;
-  const int kre = (metric == MEMSHARE_METRIC_EUCLIDEAN && kAnchors == 1 && MS_PIPE && mode != MEMSHARE_DIST_FINALIZE)
-                      ? st_kre(slice_bytes, &st_nsub) : 0;
+  int kre = (kAnchors == 1 && MS_PIPE && mode != MEMSHARE_DIST_FINALIZE) ? st_kre(slice_bytes, &st_nsub) : 0;
+  if (!st_has(kre, metric)) kre = 0;
   if (kre > 0) {                                      // equal sub-slices of exactly one stage each
     a.n_sub = st_nsub;
     a.sub_bytes = kre * kChunkUnit;
@@ -1370,7 +1417,7 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   while (plan_np2 < target_cap && plan_np2 < kPlanSortCap) plan_np2 <<= 1;
   if (kAnchors > 1) launch_pdl(plan_kernel, dim3(1), dim3(kPlanThreads), (size_t)plan_np2 * sizeof(unsigned long long), st, a);
   if (kre > 0) {
-    if (launch_st_any(kre, a, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+    if (launch_st_any(kre, metric, a, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   } else if (metric == MEMSHARE_METRIC_COSINE)
     launch_pdl(distance_kernel<MEMSHARE_METRIC_COSINE>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
   else
