@@ -88,12 +88,14 @@ __device__ __forceinline__ int64_t block_sum(int64_t v, int64_t* sh) {
   return t;
 }
 
-// "Last CTA done" election for fused count -> scan kernels. All threads call it.
+// "Last CTA done" election for fused count -> scan kernels. All threads call it. The CTA's writes
+// are ordered before the counter update by the barrier plus ONE cumulative gpu-scope fence in the
+// electing thread (not a fence in every thread: that is a MEMBAR + L1 invalidate per thread).
 __device__ __forceinline__ bool last_block_done(unsigned int* ctr) {
   __shared__ bool last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence();
     const unsigned int prev = atomicAdd(ctr, 1u);
     last = (prev == gridDim.x - 1);
   }
