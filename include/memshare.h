@@ -269,6 +269,12 @@ const char* memshare_status_string(memshare_status status);
 /* MEMSHARE_ABI_VERSION of the loaded library. */
 int32_t memshare_abi_version(void);
 
+/* Profiling hook (measurement only): when begin/end are non-NULL cudaEvent_t handles, every
+ * subsequent memshare_block_distance call on this host thread records `begin` immediately before
+ * and `end` immediately after its streaming kernel, on the call's stream, so the kernel's
+ * device time can be read apart from the finalisation; NULL, NULL turns it off. */
+void memshare_profile_distance_events(void* begin, void* end);
+
 /* memshare_block_distance_finalize_peers -- FINALIZE for the KV-head-sharded mode with the
  * cross-rank reduction fused in (reading R17): instead of an all-reduce of the
  * PARTIAL squared sums followed by FINALIZE, each rank's finalisation loads every rank's

@@ -88,6 +88,8 @@ def _load():
     L.memshare_admit.restype = I32
     L.memshare_status_string.argtypes = [I32]
     L.memshare_status_string.restype = ctypes.c_char_p
+    L.memshare_profile_distance_events.argtypes = [P, P]
+    L.memshare_profile_distance_events.restype = None
     L.memshare_abi_version.argtypes = []
     L.memshare_abi_version.restype = I32
     return L
@@ -115,6 +117,13 @@ def check(code: int, what: str = "memshare"):
     if code != OK:
         raise MemShareError(f"{what}: {status_string(code)}")
     return code
+
+
+def profile_distance_events(begin, end):
+    """Measurement hook: record torch.cuda.Event begin/end around the streaming kernel of every
+    following block_distance call on this thread (None, None: off)."""
+    lib.memshare_profile_distance_events(None if begin is None else ctypes.c_void_p(begin.cuda_event),
+                                         None if end is None else ctypes.c_void_p(end.cuda_event))
 
 
 def abi_version() -> int:

@@ -1308,6 +1308,13 @@ static int32_t n_sub_ws(int64_t slice_bytes) {
   return (st_kre(slice_bytes, &ns) > 0 && ns > g) ? ns : g;
 }
 
+static thread_local cudaEvent_t g_prof_begin = nullptr, g_prof_end = nullptr;
+
+extern "C" void memshare_profile_distance_events(void* begin, void* end) {
+  g_prof_begin = static_cast<cudaEvent_t>(begin);
+  g_prof_end = static_cast<cudaEvent_t>(end);
+}
+
 extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* dims, int32_t num_blocks,
                                                          int64_t pair_cap, int64_t target_cap, int32_t metric) {
   if (!dims || pair_cap < 0 || target_cap < 0 || num_blocks < 0 || dims->num_layers < 1) return 0;
@@ -1416,12 +1423,15 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   int64_t plan_np2 = 1;
   while (plan_np2 < target_cap && plan_np2 < kPlanSortCap) plan_np2 <<= 1;
   if (kAnchors > 1) launch_pdl(plan_kernel, dim3(1), dim3(kPlanThreads), (size_t)plan_np2 * sizeof(unsigned long long), st, a);
+  const bool prof = g_prof_begin != nullptr && g_prof_end != nullptr;
+  if (prof && cudaEventRecord(g_prof_begin, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   if (kre > 0) {
     if (launch_st_any(kre, metric, a, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   } else if (metric == MEMSHARE_METRIC_COSINE)
     launch_pdl(distance_kernel<MEMSHARE_METRIC_COSINE>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
   else
     launch_pdl(distance_kernel<MEMSHARE_METRIC_EUCLIDEAN>, dim3(sm_count()), dim3(kThreads), sizeof(DistSmem), st, a);
+  if (prof && cudaEventRecord(g_prof_end, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 0);
   return launch_status();
 }
