@@ -268,10 +268,17 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # MEMSHARE_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, to exercise the
+    # multi-rank code path (barriers, max-over-ranks timing, pair sums) on a one-GPU box
+    shared_gpu = os.environ.get("MEMSHARE_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared_gpu else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2507_21433_b200 import _lib as L
     from paper_2507_21433_b200.pipeline import MemSharePath
 
@@ -338,7 +345,7 @@ def main():
     for fn in (front, middle, back):      # eager warm-up (module load, attributes)
         fn()
     torch.cuda.synchronize()
-    if args.no_graph or collective == "p2p":     # symmetric-memory barriers run eagerly
+    if args.no_graph or collective != "none":    # collectives / symmetric-memory barriers run eagerly
         run = (front, middle, back)
     else:                                  # one CUDA graph per phase; events between replays
         run = tuple(path.capture(fn).replay for fn in (front, middle, back))
@@ -383,7 +390,7 @@ def main():
         restore()
         torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     time.sleep(0.3)
     d_events = [(ev(), ev()) for _ in range(args.steps)]
     if world > 1:
