@@ -111,6 +111,16 @@ def test_randomized_configurations(seed):
         full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=[oracle.CUR_ALL, oracle.CUR_LAST][mode])
 
 
+@pytest.mark.parametrize("shape", [kv.KVShape(2, 3, 64, 16), kv.KVShape(2, 12, 128, 16), kv.KVShape(2, 20, 128, 16),
+                                   kv.KVShape(3, 1, 8, 16), kv.KVShape(2, 9, 128, 16)])
+def test_stage_geometries(shape):
+    """Slice sizes off the configs' grid: 6 KiB and 256 B (not 4 KiB multiples: generic kernel),
+    48 KiB (two 24 KiB stages), 80 KiB (two 40 KiB stages), 36 KiB (one 36 KiB stage)."""
+    w = workloads.small(shape, 2, 1800, seed=shape.num_kv_heads)
+    full_parity(w, tau_s=0.6, pairing=oracle.CROSS)
+    full_parity(w)
+
+
 def test_online_modes():
     """LAST with 3 sequences runs Stage 1 as 8-CTA clusters per current step (DSMEM sum of the
     ranks' partial dots); RANGE runs one CTA per step."""
