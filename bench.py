@@ -601,6 +601,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "distance_st_kernel (memshare_block_distance)",
                      "kernel_ms": d_ms, "kernel_share_of_step": d_ms / ms_step, "algorithmic_bytes": alg_bytes,
+                     "pairs_per_s_a5a6": P / (d_ms / 1e3),
                      "kv_bytes": kv_bytes, "distinct_blocks": U, "peak_source": peak_src,
                      "frac_of_nominal_8000": achieved / 8000.0,
                      "note": "achieved/kernel_ms: CUDA events around the whole a5-a6 call inside the timed loop "
