@@ -176,6 +176,7 @@ __device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {
   return lo;
 }
 
+// One CTA per step (latency-optimal when the steps fit in one wave: a single CoT).
 __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   pdl_trigger();
   pdl_wait();
@@ -204,6 +205,78 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
       a.ws.step_seq[g] = s;
     }
     __syncthreads();
+  }
+}
+
+// One WARP per step (8 steps per CTA in flight): the step's {key, count} table lives in the
+// warp's 1024-slot slice of shared memory (steps of <= 256 content tokens: load <= 0.25) or in the
+// step's private region of the global workspace; n2 = sum of count^2 (int64, exact).
+constexpr int kEncSlots = kSmemSlots / kNW;                // 1024 slots per warp
+
+__device__ int64_t warp_step_n2(const CandArgs& a, int2* s_tab, const int32_t* t, int64_t tok_base, int32_t start,
+                                int32_t end, int32_t nbag) {
+  const int lane = threadIdx.x & 31;
+  int2* slots;
+  uint32_t cap;
+  bool global;
+  if (nbag <= kEncSlots / 4) {
+    cap = pow2_ceil(4u * (uint32_t)(nbag > 32 ? nbag : 32));
+    slots = s_tab;
+    global = false;
+  } else {
+    cap = pow2_floor(4u * (uint32_t)(end - start));
+    slots = a.ws.gtab + 4 * (tok_base + start);
+    global = true;
+  }
+  const uint32_t mask = cap - 1, shift = 32u - (31u - __clz(cap));
+  for (uint32_t i = lane; i < cap; i += 32) slots[i] = make_int2(kEmpty, 0);
+  if (global) __threadfence_block();
+  __syncwarp();
+  for (int32_t p = start + lane; p < end; p += 32) {
+    const int32_t tok = t[p];
+    if (is_delim(tok, a.dl)) continue;
+    uint32_t slot = hash_slot(tok, shift);
+    for (uint32_t probe = 0; probe <= mask; ++probe) {
+      const int32_t prev = atomicCAS(&slots[slot].x, kEmpty, tok);
+      if (prev == kEmpty || prev == tok) {
+        atomicAdd(&slots[slot].y, 1);
+        break;
+      }
+      slot = (slot + 1) & mask;
+    }
+  }
+  if (global) __threadfence_block();
+  __syncwarp();
+  int64_t n2 = 0;
+  for (uint32_t i = lane; i < cap; i += 32) {
+    const int64_t c = global ? __ldcg(slots + i).y : slots[i].y;
+    n2 += c * c;
+  }
+  return warp_sum(n2);
+}
+
+__global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ int2 s_tab[];                         // [kSmemSlots] = kNW warps x kEncSlots
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t G = total_steps(a);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
+    *a.ws.done = 0u;
+    *a.ws.stash_alloc = 0ull;
+  }
+  for (int64_t g = (int64_t)blockIdx.x * kNW + w; g < G; g += (int64_t)gridDim.x * kNW) {
+    const int32_t s = seq_of_step(a, g);
+    const int64_t tok_base = a.seq_tok_off[s];
+    const int32_t nbag = a.step_nbag[g];
+    const int64_t n2 = nbag > 0 ? warp_step_n2(a, s_tab + w * kEncSlots, a.tokens + tok_base, tok_base,
+                                               a.step_start[g], a.step_end[g], nbag)
+                                : 0;
+    if (lane == 0) {
+      a.ws.n2[g] = n2;
+      a.ws.step_seq[g] = s;
+    }
+    __syncwarp();
   }
 }
 
@@ -807,14 +880,23 @@ extern "C" memshare_status memshare_step_candidates(
   if (!attr_set) {
     cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem));
     cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemSlots * sizeof(int2)));
+    cudaFuncSetAttribute(encode_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kSmemSlots * sizeof(int2)));
     cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FillSmem));
     attr_set = true;
   }
   const int sms = sm_count();
   const int64_t gcap = step_cap < 1 ? 1 : step_cap;
-  const int grid_enc = (int)(gcap < 8 * sms ? gcap : 8 * sms);
+  // a2 encode: one CTA per step while the steps (~1 per 100 tokens) fit in 8 waves of CTAs,
+  // one warp per step beyond (large batches: 8 steps in flight per CTA)
+  const bool enc_warp = num_tokens > (int64_t)100 * 8 * sms;
+  const int64_t enc_ctas = enc_warp ? (gcap + kNW - 1) / kNW : gcap;
+  const int grid_enc = (int)(enc_ctas < 8 * sms ? enc_ctas : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
-  launch_pdl(encode_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
+  if (enc_warp)
+    launch_pdl(encode_warp_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
+  else
+    launch_pdl(encode_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
   {
     // cluster size per current step: online rounds (LAST: one current step per sequence) split
     // each step's history over up to 8 CTAs while the clusters still fit in one wave; offline
