@@ -133,10 +133,10 @@ struct Table {
 };
 
 __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, int64_t tok_base, int32_t start,
-                             int32_t end, int32_t nbag) {
+                             int32_t end, int32_t nbag, int32_t smem_slots = kSmemSlots) {
   Table tb;
   uint32_t cap;
-  if (nbag <= kSmemSlots / 4) {
+  if (nbag <= smem_slots / 4) {
     cap = pow2_ceil(4u * (uint32_t)(nbag > 32 ? nbag : 32));
     tb.slots = s_tab;
     tb.global = false;
@@ -435,8 +435,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
       g_dbg_t[blockIdx.x * kDbgSlots + (slot)] = gtimer();                                  \
   } while (0)
 
+// Stage-1 CTA shapes: 1024 threads, one CTA per SM (a single CoT / online rounds: the widest
+// history stream per step), or 512 threads with half the table and staging, two CTAs per SM
+// (large batches: two steps in flight per SM hide each other's latency-bound phases).
+template <int NT>
+struct S1Cfg {
+  static constexpr int kSlots = NT == 1024 ? kSmemSlots : kSmemSlots / 2;
+  static constexpr int kTok = NT == 1024 ? kHistTok : kHistTok / 2;
+};
+
+template <int NT>
 struct SelSmem {
-  int2 tab[kSmemSlots];
+  int2 tab[S1Cfg<NT>::kSlots];
   double cs[kCandCap];
   int32_t js[kCandCap];
   int32_t jasc[kCandCap];
@@ -445,10 +455,10 @@ struct SelSmem {
   int32_t cum[kCandCap + 1];
   int32_t hst[kChunk];
   int32_t hen[kChunk];
-  int32_t tok[kHistTok];   // staged history tokens
+  int32_t tok[S1Cfg<NT>::kTok];   // staged history tokens
   uint32_t dot_lo[kChunk];
   uint32_t dot_hi[kChunk];
-  int64_t sh[kNW1 + 1];
+  int64_t sh[NT / 32 + 1];
   int count;
   int overflow;
   uint32_t acc_t;
@@ -465,7 +475,7 @@ __device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, u
                                                int32_t dn, const Delims& dl, const int32_t* s_tok, int32_t clo,
                                                int32_t chi, bool dbg_noprobe) {
   const int32_t n = chi - clo;
-  const int32_t per = (n + kNT1 - 1) / kNT1;                // tokens per thread
+  const int32_t per = (n + (int32_t)blockDim.x - 1) / (int32_t)blockDim.x;   // tokens per thread
   int32_t p = clo + (int32_t)threadIdx.x * per;
   const int32_t pe = (p + per < chi) ? p + per : chi;
   if (p >= pe) return;
@@ -502,9 +512,10 @@ __device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, u
 
 // One-CTA exclusive scans of the per-step match / target / pair counts (one pass, one set of
 // barriers: the three int32 counts of a step travel packed as 3 x 21 bits when they fit).
+template <int NT>
 __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
   int64_t cm = 0, ct = 0, cp = 0;
-  for (int64_t base = 0; base < G; base += kNT1) {
+  for (int64_t base = 0; base < G; base += NT) {
     const int64_t i = base + threadIdx.x;
     int64_t m = 0, t = 0, p = 0;
     if (i < G) { m = __ldcg(a.ws.cnt_m + i); t = __ldcg(a.ws.cnt_t + i); p = __ldcg(a.ws.cnt_p + i); }
@@ -513,7 +524,7 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
     const bool packed = m < 2048 && t < 2048 && p < 2048;
     const int all_packed = __syncthreads_and(packed);
     if (all_packed) {
-      const int64_t ex = block_excl_scan<kNT1>(m | (t << 21) | (p << 42), tot, sh);
+      const int64_t ex = block_excl_scan<NT>(m | (t << 21) | (p << 42), tot, sh);
       if (i < G) {
         a.ws.off_m[i] = cm + (ex & 0x1FFFFF);
         a.ws.off_t[i] = ct + ((ex >> 21) & 0x1FFFFF);
@@ -521,13 +532,13 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
       }
       cm += tot & 0x1FFFFF; ct += (tot >> 21) & 0x1FFFFF; cp += tot >> 42;
     } else {
-      const int64_t exm = block_excl_scan<kNT1>(m, tot, sh);
+      const int64_t exm = block_excl_scan<NT>(m, tot, sh);
       if (i < G) a.ws.off_m[i] = cm + exm;
       cm += tot;
-      const int64_t ext = block_excl_scan<kNT1>(t, tot, sh);
+      const int64_t ext = block_excl_scan<NT>(t, tot, sh);
       if (i < G) a.ws.off_t[i] = ct + ext;
       ct += tot;
-      const int64_t exp_ = block_excl_scan<kNT1>(p, tot, sh);
+      const int64_t exp_ = block_excl_scan<NT>(p, tot, sh);
       if (i < G) a.ws.off_p[i] = cp + exp_;
       cp += tot;
     }
@@ -535,11 +546,13 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
   if (threadIdx.x == 0) { a.ws.off_m[G] = cm; a.ws.off_t[G] = ct; a.ws.off_p[G] = cp; }
 }
 
-__global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
+  constexpr int kNTs = NT, kNWs = NT / 32;
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SelSmem& sm = *reinterpret_cast<SelSmem*>(smem_raw);
+  SelSmem<NT>& sm = *reinterpret_cast<SelSmem<NT>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // Thread-block cluster of csize CTAs per current step (online rounds: few current steps, long
   // histories): every rank builds the step's table, streams 1/csize of the history into its own
@@ -555,7 +568,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
   // dependent loads per skipped step).
   const bool last_mode = a.cur_mode == MEMSHARE_CUR_LAST;
   if (last_mode) {
-    for (int64_t g = (int64_t)blockIdx.x * kNT1 + threadIdx.x; g < G; g += (int64_t)gridDim.x * kNT1) {
+    for (int64_t g = (int64_t)blockIdx.x * kNTs + threadIdx.x; g < G; g += (int64_t)gridDim.x * kNTs) {
       const int32_t s = a.ws.step_seq[g];
       if (g != a.seq_step_off[s + 1] - 1) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
     }
@@ -575,7 +588,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
     }
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t* t = a.tokens + tok_base;
-    const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag);
+    const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots);
     DBG_T(1);
     const double n2k = (double)a.ws.n2[g];
     if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
@@ -587,7 +600,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
     for (int64_t jb = 0; jb < k; jb += kChunk) {
       const int64_t je = (jb + kChunk < k) ? jb + kChunk : k;
       const int nj = (int)(je - jb);
-      for (int i = threadIdx.x; i < nj; i += kNT1) {
+      for (int i = threadIdx.x; i < nj; i += kNTs) {
         sm.hst[i] = a.step_start[gfirst + jb + i];
         sm.hen[i] = a.step_end[gfirst + jb + i];
         sm.dot_lo[i] = 0u;
@@ -600,11 +613,11 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
       const int32_t lo0 = sm.hst[0], hi0 = sm.hen[nj - 1];
       const int32_t lo = lo0 + (int32_t)((int64_t)(hi0 - lo0) * crank / csize);      // this rank's share
       const int32_t hi = lo0 + (int32_t)((int64_t)(hi0 - lo0) * (crank + 1) / csize);
-      for (int32_t clo = lo; clo < hi; clo += kHistTok) {
-        const int32_t chi = (hi - clo > kHistTok) ? clo + kHistTok : hi;
+      for (int32_t clo = lo; clo < hi; clo += S1Cfg<NT>::kTok) {
+        const int32_t chi = (hi - clo > S1Cfg<NT>::kTok) ? clo + S1Cfg<NT>::kTok : hi;
         // coalesced, independent loads: one memory latency for the whole pass
 #pragma unroll 4
-        for (int32_t i = threadIdx.x; i < chi - clo; i += kNT1) sm.tok[i] = __ldg(t + clo + i);
+        for (int32_t i = threadIdx.x; i < chi - clo; i += kNTs) sm.tok[i] = __ldg(t + clo + i);
         __syncthreads();
         if (jb == 0 && clo == lo) DBG_T(14);
         if (!(a.dbg_skip & 1)) {
@@ -621,7 +634,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
       if (csize > 1) {
         cl.sync();                                         // every rank's partial dots are final
         if (crank == 0) {
-          for (int i = threadIdx.x; i < nj; i += kNT1) {
+          for (int i = threadIdx.x; i < nj; i += kNTs) {
             uint64_t d = ((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i];
             for (int r = 1; r < csize; ++r) {
               const uint32_t* rl = cl.map_shared_rank(sm.dot_lo, r);
@@ -638,7 +651,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
       if (jb == 0) DBG_T(11);
       if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
         g_dbg_t[blockIdx.x * kDbgSlots + 13] = clock64();
-      for (int i = threadIdx.x; i < nj; i += kNT1) {
+      for (int i = threadIdx.x; i < nj; i += kNTs) {
         const int64_t gj = gfirst + jb + i;
         if (a.step_nbag[gj] == 0) continue;                // void history step (reading R5)
         const int64_t dot = (int64_t)(((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i]);
@@ -676,7 +689,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
     }
     __syncthreads();
     const int64_t base = (int64_t)s_base;
-    for (int r = threadIdx.x; r < m; r += kNT1) {
+    for (int r = threadIdx.x; r < m; r += kNTs) {
       if (base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
       sm.jasc[r] = sm.js[r];
     }
@@ -692,7 +705,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
     if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
     const int32_t* trow = a.table + (int64_t)s * a.table_stride;
     int64_t my_t = 0, my_p = 0;
-    for (int32_t i = w; i < nt && !(a.dbg_skip & 2); i += kNW1) {
+    for (int32_t i = w; i < nt && !(a.dbg_skip & 2); i += kNWs) {
       const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
       my_t += kept > 0 ? 1 : 0;
       my_p += kept;
@@ -711,7 +724,7 @@ __global__ void __launch_bounds__(kNT1, 1) stage1_kernel(CandArgs a) {
   DBG_T(7);
   if (!(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
     DBG_T(8);
-    scan_counts3(a, G, sm.sh);
+    scan_counts3<NT>(a, G, sm.sh);
     __syncthreads();
     if (threadIdx.x == 0) {
       const int64_t M = a.ws.off_m[G], T = a.ws.off_t[G], P = a.ws.off_p[G];
@@ -878,7 +891,8 @@ extern "C" memshare_status memshare_step_candidates(
   static bool attr_set_dev[kMaxDevices] = {};
   bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
-    cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem));
+    cudaFuncSetAttribute(stage1_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem<1024>));
+    cudaFuncSetAttribute(stage1_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem<512>));
     cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemSlots * sizeof(int2)));
     cudaFuncSetAttribute(encode_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(kSmemSlots * sizeof(int2)));
@@ -909,11 +923,16 @@ extern "C" memshare_status memshare_step_candidates(
       for (int c = 8; c > 1; c >>= 1)
         if ((int64_t)num_seqs * c <= sms) { cs = c; break; }
     if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
-    const int ncl = (int)((gcap < sms / cs) ? gcap : sms / cs);
+    // large batches without clusters: 512-thread CTAs, two per SM (MEMSHARE_S1_NT overrides)
+    static int env_nt = -1;
+    if (env_nt < 0) { const char* e = getenv("MEMSHARE_S1_NT"); env_nt = e ? atoi(e) : 0; }
+    const bool half = cs == 1 && (env_nt == 512 || (env_nt == 0 && enc_warp));
+    const int per_sm = half ? 2 : 1;
+    const int ncl = (int)((gcap < (int64_t)per_sm * sms / cs) ? gcap : (int64_t)per_sm * sms / cs);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(ncl * cs));
-    cfg.blockDim = dim3(kNT1);
-    cfg.dynamicSmemBytes = sizeof(SelSmem);
+    cfg.blockDim = dim3(half ? 512 : 1024);
+    cfg.dynamicSmemBytes = half ? sizeof(SelSmem<512>) : sizeof(SelSmem<1024>);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -924,7 +943,8 @@ extern "C" memshare_status memshare_step_candidates(
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (cudaLaunchKernelEx(&cfg, stage1_kernel, a) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
+      return MEMSHARE_ERR_CUDA;
   }
   launch_pdl(fill_kernel, dim3(grid_sel), dim3(kNT), sizeof(FillSmem), st, a);
   return launch_status();
