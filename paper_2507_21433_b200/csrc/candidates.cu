@@ -29,8 +29,6 @@ namespace ms {
 namespace {
 
 constexpr int kNT = 256;          // encode / fill
-constexpr int kNT1 = 1024;        // stage1 (one CTA per current step: widest history stream)
-constexpr int kNW1 = kNT1 / 32;
 constexpr int kNW = kNT / 32;
 constexpr int kSmemSlots = 8192;       // smem hash table (steps with <= 2048 content tokens, load <= 0.25)
 constexpr int kCandCap = 1024;         // survivors held per current step
