@@ -8,6 +8,13 @@
  *                                  threshold and the per-target selection       :267-269, :319-320
  *   memshare_remap            a7   zero-copy sharing: block-table rewrite,
  *                                  refcounts, free list
+ * plus, around the path:
+ *   memshare_block_distance_finalize_peers   KV-head-sharded FINALIZE reading every rank's
+ *                                  partial sums over NVLink (the fused cross-rank reduction)
+ *   memshare_kv_append / memshare_paged_attention_decode / memshare_admit   f1 decode loop:
+ *                                  append, attention through the (remapped) table, admission
+ *   memshare_similarity_ratio / memshare_all_pairs   f4 / f3 analysis on the same machinery
+ *   memshare_profile_distance_events   measurement hook (events around the streaming kernel)
  *
  * Conventions (all calls):
  *  - Pointers named *_host are host memory; every other pointer is DEVICE memory (cudaMalloc /
