@@ -147,6 +147,50 @@ def test_phi4_shape_sub_slices():
     full_parity(w)
 
 
+def test_degenerate_rounds():
+    """Rounds with nothing to share: tau_s = 1.0 (strict 'exceeding' can never hold) gives no
+    match, no pair, no target -- the distance call and the remap are no-ops and the table,
+    refcounts and free list come back unchanged; a trace without any delimiter has no finished
+    step unless it is final."""
+    import torch
+    w = workloads.small(SMALL, 2, 2000, seed=3)
+    p = make_path(w)
+    s0 = p.read_state()
+    p.round(1.0, w.tau_b)
+    torch.cuda.synchronize()
+    assert p.read_status() == 0
+    assert p.counts()["pairs"] == 0 and p.counts()["targets"] == 0 and p.counts()["matches"] == 0
+    s1 = p.read_state()
+    for k in ("table", "refcount", "free_list"):
+        assert np.array_equal(s0[k], s1[k]), k
+    assert s1["num_freed"] == 0 and s1["affected"] == 0 and s1["free_count"] == s0["free_count"]
+    # no delimiter at all: one step per FINAL sequence, none for an open one
+    b = w.batch
+    toks = np.full(3000, 7, np.int32)
+    off = np.asarray([0, 1500, 3000], np.int64)
+    for fin in ([1, 0], [0, 0]):
+        exp = oracle.segment_steps(toks, off, np.zeros(2, np.int32), np.asarray(fin, np.uint8), b.delim_ids)
+        assert exp["seq_step_off"][-1] == sum(fin)
+        pp = MemSharePathFor(toks, off, fin, b.delim_ids, w)
+        pp.segment()
+        pp.candidates(-1.0)
+        torch.cuda.synchronize()
+        assert pp.read_status() == 0 and pp.counts()["steps"] == sum(fin) and pp.counts()["pairs"] == 0
+
+
+def MemSharePathFor(toks, off, fin, delims, w):
+    from paper_2507_21433_b200.pipeline import MemSharePath
+    S = off.size - 1
+    nb = int(sum(-(-(off[i + 1] - off[i]) // 16) for i in range(S)))
+    table = np.arange(nb, dtype=np.int32).reshape(S, -1) if nb % S == 0 else None
+    assert table is not None
+    rc = np.ones(nb, np.int32)
+    fl = np.full(nb, -1, np.int32)
+    return MemSharePath(toks, off, np.zeros(S, np.int32), np.asarray(fin, np.uint8), delims, table, rc, fl, 0, None,
+                        None, 0, 0, nb, SMALL.num_layers, SMALL.num_kv_heads, SMALL.num_kv_heads, SMALL.head_dim,
+                        SMALL.block_size)
+
+
 def test_segment_edge_cases():
     """Ragged, empty, non-final, prompt-only, delimiter-only, multi-delimiter and multi-tile
     sequences, against the oracle."""
