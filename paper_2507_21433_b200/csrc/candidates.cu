@@ -52,6 +52,9 @@ struct CandWs {
   double* stash_cos;     // [match_cap]
   int32_t* stash_j;
   int2* gtab;            // [4*num_tokens] {key, count} global tables of oversize steps
+  int32_t* lb_flag;      // [step_cap] fused fill: 0 none, 1 aggregate, 2 inclusive prefix (zeroed by encode)
+  int4* lb_agg;          // [step_cap] {matches, targets, pairs} of the step
+  int4* lb_inc;          // [step_cap] inclusive prefix through the step
 };
 
 CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_cap) {
@@ -70,6 +73,9 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   c.stash_cos = w.take<double>(match_cap + 1);
   c.stash_j = w.take<int32_t>(match_cap + 1);
   c.gtab = w.take<int2>(4 * num_tokens + 1);
+  c.lb_flag = w.take<int32_t>(step_cap + 1);
+  c.lb_agg = w.take<int4>(step_cap + 1);
+  c.lb_inc = w.take<int4>(step_cap + 1);
   return c;
 }
 
@@ -103,6 +109,7 @@ struct CandArgs {
   int64_t target_cap;
   int64_t* num_targets;
   int32_t* status;
+  int32_t fused;        // offline single-CoT launch: stage1 writes matches / pairs itself (no fill kernel)
   int32_t dbg_skip;     // tuning only (env MEMSHARE_DEBUG_SKIP): bit0 history stream, bit1 pair count, bit2 last-CTA scan
   CandWs ws;
 };
@@ -181,6 +188,8 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   extern __shared__ int2 s_tab[];                         // [kSmemSlots]
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
+    a.ws.lb_flag[g] = 0;                                  // stage1's look-back flags (fused fill)
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
@@ -259,6 +268,8 @@ __global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
   extern __shared__ int2 s_tab[];                         // [kSmemSlots] = kNW warps x kEncSlots
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t G = total_steps(a);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
+    a.ws.lb_flag[g] = 0;                                  // stage1's look-back flags (fused fill)
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
@@ -453,7 +464,7 @@ struct SelSmem {
   int32_t cum[kCandCap + 1];
   int32_t hst[kChunk];
   int32_t hen[kChunk];
-  int32_t tok[S1Cfg<NT>::kTok];   // staged history tokens
+  alignas(16) int32_t tok[S1Cfg<NT>::kTok];   // staged history tokens (fused fill: reused, needs 8 B alignment)
   uint32_t dot_lo[kChunk];
   uint32_t dot_hi[kChunk];
   int64_t sh[NT / 32 + 1];
@@ -544,9 +555,84 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
   if (threadIdx.x == 0) { a.ws.off_m[G] = cm; a.ws.off_t[G] = ct; a.ws.off_p[G] = cp; }
 }
 
+__device__ __forceinline__ int32_t s1_ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void s1_st_release(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Fused fill (offline, one CTA per step in one wave): step g publishes its {matches, targets,
+// pairs} counts and obtains the exclusive prefix over steps < g by a decoupled look-back (warp 0,
+// 32 predecessors per window; every step publishes its aggregate before it waits, and steps are
+// taken in ascending order by co-resident CTAs, so the waits always end). Returns the prefix to
+// every thread of the CTA.
+__device__ int4 s1_lookback(const CandArgs& a, int64_t g, int32_t m, int32_t t, int32_t p, int4* s_out) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    if (g == 0) {
+      if (lane == 0) {
+        a.ws.lb_inc[0] = make_int4(m, t, p, 0);
+        __threadfence();
+        s1_st_release(a.ws.lb_flag, 2);
+        *s_out = make_int4(0, 0, 0, 0);
+      }
+    } else {
+      if (lane == 0) {
+        a.ws.lb_agg[g] = make_int4(m, t, p, 0);
+        __threadfence();
+        s1_st_release(a.ws.lb_flag + g, 1);
+      }
+      int32_t rm = 0, rt = 0, rp = 0;
+      for (int64_t q0 = g - 1;; q0 -= 32) {
+        const int64_t q = q0 - lane;
+        int32_t f = 2;
+        if (q >= 0) {
+          while ((f = s1_ld_acquire(a.ws.lb_flag + q)) == 0) {
+          }
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 32;           // nearest predecessor with a prefix
+        int4 v = make_int4(0, 0, 0, 0);
+        if (q >= 0 && lane < stop) v = __ldcg(a.ws.lb_agg + q);
+        else if (q >= 0 && lane == stop) v = __ldcg(a.ws.lb_inc + q);
+        if (lane > stop) v = make_int4(0, 0, 0, 0);
+        rm += warp_sum(v.x);
+        rt += warp_sum(v.y);
+        rp += warp_sum(v.z);
+        if (stop < 32) break;
+      }
+      if (lane == 0) {
+        a.ws.lb_inc[g] = make_int4(rm + m, rt + t, rp + p, 0);
+        __threadfence();
+        s1_st_release(a.ws.lb_flag + g, 2);
+        *s_out = make_int4(rm, rt, rp, 0);
+      }
+    }
+  }
+  __syncthreads();
+  return *s_out;
+}
+
+// the last step's CTA: totals and target_off[T]
+__device__ void s1_totals(const CandArgs& a, int4 incl) {
+  if (threadIdx.x == 0) {
+    const int64_t M = incl.x, T = incl.y, P = incl.z;
+    *a.num_matches = M;
+    *a.num_targets = T;
+    *a.num_pairs = P;
+    if (M > a.match_cap || T > a.target_cap || P > a.pair_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+    if (T <= a.target_cap) a.target_off[T] = P;
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   constexpr int kNTs = NT, kNWs = NT / 32;
+  static_assert(NT != 1024 || kMaxTgt * 16 <= S1Cfg<1024>::kTok * 4, "fused fill reuses the staging area");
+  const bool fused = NT == 1024 && a.fused != 0;   // the 512-thread shape never fuses
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -561,6 +647,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   const int64_t cid = blockIdx.x / csize, ncl = gridDim.x / csize;
   DBG_T(0);
   const int64_t G = total_steps(a);
+  __shared__ int4 s_lb;
+  if (fused && G == 0 && blockIdx.x == 0) s1_totals(a, make_int4(0, 0, 0, 0));
   // LAST (online): the work list is one step per sequence, found directly; the counts of every
   // other step are zeroed up front by all threads (one parallel pass instead of a chain of
   // dependent loads per skipped step).
@@ -582,6 +670,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     const int32_t nbag = a.step_nbag[g];
     if (nbag == 0 || !is_current(a, s, k, S)) {
       if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
+      if (fused) {
+        if (g == G - 1) {
+          const int4 pre = s1_lookback(a, g, 0, 0, 0, &s_lb);
+          s1_totals(a, pre);
+        } else if (threadIdx.x == 0) {
+          if (g == 0) { a.ws.lb_inc[0] = make_int4(0, 0, 0, 0); __threadfence(); s1_st_release(a.ws.lb_flag, 2); }
+          else { a.ws.lb_agg[g] = make_int4(0, 0, 0, 0); __threadfence(); s1_st_release(a.ws.lb_flag + g, 1); }
+        }
+      }
       continue;
     }
     const int64_t tok_base = a.seq_tok_off[s];
@@ -682,13 +779,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     // stash the ranked survivors for the fill kernel
     __shared__ unsigned long long s_base;
     if (threadIdx.x == 0) {
-      s_base = m > 0 ? atomicAdd(a.ws.stash_alloc, (unsigned long long)m) : 0ull;
-      if ((int64_t)(s_base + m) > a.match_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+      s_base = (m > 0 && !fused) ? atomicAdd(a.ws.stash_alloc, (unsigned long long)m) : 0ull;
+      if (!fused && (int64_t)(s_base + m) > a.match_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
     }
     __syncthreads();
     const int64_t base = (int64_t)s_base;
     for (int r = threadIdx.x; r < m; r += kNTs) {
-      if (base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
+      if (!fused && base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
       sm.jasc[r] = sm.js[r];
     }
     if (threadIdx.x == 0) { sm.acc_t = 0u; sm.acc_p = 0u; }
@@ -703,10 +800,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
     const int32_t* trow = a.table + (int64_t)s * a.table_stride;
     int64_t my_t = 0, my_p = 0;
+    // fused fill: the history staging area is free now; it holds the per-target kept counts,
+    // pair offsets and target numbers of the step (kMaxTgt x 16 B = 64 KiB)
+    int32_t* f_tc = reinterpret_cast<int32_t*>(sm.tok);
+    int64_t* f_tpos = reinterpret_cast<int64_t*>(f_tc + kMaxTgt);
+    int32_t* f_tnum = reinterpret_cast<int32_t*>(f_tpos + kMaxTgt);
     for (int32_t i = w; i < nt && !(a.dbg_skip & 2); i += kNWs) {
       const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
       my_t += kept > 0 ? 1 : 0;
       my_p += kept;
+      if (fused && lane == 0 && i < kMaxTgt) f_tc[i] = kept;
     }
     if (lane == 0) { atomicAdd(&sm.acc_t, (uint32_t)my_t); atomicAdd(&sm.acc_p, (uint32_t)my_p); }
     __syncthreads();
@@ -718,9 +821,45 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
       a.ws.stash_base[g] = base;
     }
     __syncthreads();
+    if (fused) {
+      // offsets of this step's outputs, then the fill kernel's work done here
+      const int4 pre = s1_lookback(a, g, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
+      if (g == G - 1) s1_totals(a, make_int4(pre.x + m, pre.y + (int32_t)sm.acc_t, pre.z + (int32_t)sm.acc_p, 0));
+      const int64_t mo = pre.x, to = pre.y, po = pre.z;
+      for (int r = threadIdx.x; r < m; r += kNTs) {
+        if (mo + r < a.match_cap) {
+          memshare_step_match mt;
+          mt.seq = s; mt.step = (int32_t)k; mt.cand_step = sm.js[r]; mt.rank = r; mt.cosine = sm.cs[r];
+          a.matches[mo + r] = mt;
+        }
+      }
+      const int32_t ntf = nt < kMaxTgt ? nt : kMaxTgt;
+      int64_t pcarry = 0, tcarry = 0;
+      for (int32_t ib = 0; ib < ntf; ib += kNTs) {
+        const int32_t i = ib + threadIdx.x;
+        const int64_t v = i < ntf ? f_tc[i] : 0;
+        int64_t tot;
+        const int64_t ex = block_excl_scan<NT>(v, tot, sm.sh);
+        int64_t tt;
+        const int64_t tex = block_excl_scan<NT>(v > 0 ? 1 : 0, tt, sm.sh);
+        if (i < ntf) { f_tpos[i] = pcarry + ex; f_tnum[i] = v > 0 ? (int32_t)(tcarry + tex) : -1; }
+        pcarry += tot;
+        tcarry += tt;
+      }
+      __syncthreads();
+      for (int32_t i = w; i < ntf; i += kNWs) {
+        if (f_tnum[i] < 0) continue;
+        const int64_t tidx = to + f_tnum[i];
+        const int32_t tl = fk_lo + i;
+        const int32_t tphys = phys_of(a, trow, tl);
+        target_sources(a, c, trow, s, i, tl, tphys, (int32_t)tidx, a.pairs, po + f_tpos[i], a.pair_cap);
+        if (lane == 0 && tidx < a.target_cap) a.target_off[tidx] = po + f_tpos[i];
+      }
+      __syncthreads();
+    }
   }
   DBG_T(7);
-  if (!(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
+  if (!fused && !(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
     DBG_T(8);
     scan_counts3<NT>(a, G, sm.sh);
     __syncthreads();
@@ -838,6 +977,12 @@ extern "C" size_t memshare_step_candidates_workspace_size(int64_t num_tokens, in
   return w.size();
 }
 
+static bool fused_env() {            // MEMSHARE_FUSED_FILL=0: separate fill kernel (A/B)
+  static int on = -1;
+  if (on < 0) { const char* e = getenv("MEMSHARE_FUSED_FILL"); on = (e && e[0] == '0') ? 0 : 1; }
+  return on == 1;
+}
+
 extern "C" memshare_status memshare_step_candidates(
     const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off, int32_t num_seqs,
     const int64_t* seq_step_off, const int32_t* step_start, const int32_t* step_end, const int32_t* step_nbag,
@@ -941,9 +1086,12 @@ extern "C" memshare_status memshare_step_candidates(
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
+    // offline single-CoT shape (one 1024-thread CTA per step, no cluster): stage1 also writes the
+    // matches and pairs (look-back offsets), so no fill kernel and no last-CTA scan
+    a.fused = (cur_mode == MEMSHARE_CUR_ALL && !half && cs == 1 && fused_env()) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
   }
-  launch_pdl(fill_kernel, dim3(grid_sel), dim3(kNT), sizeof(FillSmem), st, a);
+  if (!a.fused) launch_pdl(fill_kernel, dim3(grid_sel), dim3(kNT), sizeof(FillSmem), st, a);
   return launch_status();
 }
