@@ -32,7 +32,12 @@ import numpy as np  # noqa: E402
 
 METRIC = "candidate KV-block pairs scored/s"
 UNIT = "pairs/s"
-GPU_LAUNCHES_PER_STEP = 7     # seg, encode, stage1, fill, distance, finalize, remap (our kernels; + 3 memset nodes)
+# our kernels per step: seg, encode, stage1, [fill], distance, finalize, remap (+ 2 memset nodes);
+# the fill kernel runs only when stage1 does not fuse it (the library fuses it for an offline
+# round over a single CoT-sized batch: <= 100 x 8 x SMs tokens, no cluster; MEMSHARE_FUSED_FILL=0 disables)
+def gpu_launches_per_step(num_tokens, sms=148):
+    fused = num_tokens <= 100 * 8 * sms and os.environ.get("MEMSHARE_FUSED_FILL", "1") != "0"
+    return 6 if fused else 7
 
 
 def parse():
@@ -616,7 +621,8 @@ def main():
                         if kernel_only_ms else {})},
         "per_step": {"pairs": P, "targets": T, "steps": counts["steps"], "matches": counts["matches"],
                      "freed_blocks": step_freed, "affected_tokens": step_affected},
-        "gpu_launches": GPU_LAUNCHES_PER_STEP * args.steps,
+        "gpu_launches": gpu_launches_per_step(w.num_tokens, torch.cuda.get_device_properties(dev).multi_processor_count)
+        * args.steps,
         "clocks": {"sm_mhz": ck["sm_mhz"], "sm_max_mhz": ck["sm_max_mhz"], "reasons": ck["reasons"],
                    "samples": ck["samples"]},
         "e2e": e2e, "cpu_baseline": cpu, "online": online,
