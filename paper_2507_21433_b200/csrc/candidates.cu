@@ -8,15 +8,20 @@
 // workspace for steps > 2048 content tokens). Because steps tile the sequence, the whole
 // history of k is one contiguous token range; the CTA stages it in shared memory with coalesced
 // loads, each thread walks a contiguous run, probes k's table and adds its partial dot once per
-// history step it touches (32-bit smem atomics with carry; step boundaries staged in smem). Integer dot and norms are exact; the cosine is
-// one IEEE expression (__ddiv_rn / __dsqrt_rn / __dmul_rn), bit-identical to the C oracle.
+// history step it touches (32-bit smem atomics with carry; step boundaries staged in smem).
+// Integer dot and norms are exact; the cosine is one IEEE expression (__ddiv_rn / __dsqrt_rn / __dmul_rn), bit-identical to the C oracle.
 //
-// Three launches:
-//   encode  : one CTA per step: table -> n2 = sum count^2 (history norms)
-//   stage1  : one CTA per current step: table, streamed history dots, strict threshold,
-//             (cos desc, j asc) bitonic sort, top-K, stash survivors, count targets/pairs; the
-//             last CTA scans the per-step counts into output offsets
-//   fill    : one CTA per current step: write matches, targets, target_off, pairs
+// Launches:
+//   encode  : n2 = sum count^2 per step (history norms) -- one CTA per step for a single CoT,
+//             one warp per step for large batches
+//   stage1  : per current step: table, streamed history dots, strict threshold, (cos desc, j asc)
+//             bitonic sort, top-K, count targets/pairs. Shapes: one 1024-thread CTA per step
+//             (single CoT); 512-thread CTAs two per SM (large batches); a thread-block cluster of
+//             up to 8 CTAs per step sharing its history scan over DSMEM (online LAST rounds).
+//             Offline single-CoT launches FUSE the fill: each step's CTA gets its output offsets
+//             by a decoupled look-back over the preceding steps and writes its matches and pairs.
+//             Otherwise the survivors are stashed and the last CTA scans the per-step counts.
+//   fill    : (when not fused) one CTA per current step: write matches, targets, target_off, pairs
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
