@@ -147,6 +147,36 @@ def test_phi4_shape_sub_slices():
     full_parity(w)
 
 
+@pytest.mark.parametrize("cur_mode", [oracle.CUR_ALL, oracle.CUR_LAST])
+def test_bit_reproducible_rounds(cur_mode):
+    """memshare.h: outputs are bit-reproducible run to run -- the same round twice (dynamic work
+    tickets, look-back, cluster reductions and atomics notwithstanding) gives identical matches,
+    pairs, distances, decisions and table state."""
+    import torch
+    w = workloads.small(kv.QWEN32B, 2, 2600, seed=8, gen_start=64)
+    outs = []
+    for _ in range(2):
+        p = make_path(w)
+        p.autosize(0.6, pairing=oracle.CROSS, cur_mode=cur_mode)
+        p.round(0.6, w.tau_b, pairing=oracle.CROSS, cur_mode=cur_mode)
+        torch.cuda.synchronize()
+        assert p.read_status() == 0
+        c, d, st = p.read_candidates(), p.read_distance(), p.read_state()
+        outs.append((c, d, st))
+        del p
+    (c0, d0, s0), (c1, d1, s1) = outs
+    assert c0["pairs"]["seq"].size > 0
+    for k in c0["matches"]:
+        assert np.array_equal(c0["matches"][k], c1["matches"][k]), k
+    for k in c0["pairs"]:
+        assert np.array_equal(c0["pairs"][k], c1["pairs"][k]), k
+    assert np.array_equal(d0["distance"].view(np.uint32), d1["distance"].view(np.uint32))
+    for k in d0["decisions"]:
+        assert np.array_equal(d0["decisions"][k], d1["decisions"][k]), k
+    for k in ("table", "refcount", "free_list"):
+        assert np.array_equal(s0[k], s1[k]), k
+
+
 def test_degenerate_rounds():
     """Rounds with nothing to share: tau_s = 1.0 (strict 'exceeding' can never hold) gives no
     match, no pair, no target -- the distance call and the remap are no-ops and the table,
