@@ -19,7 +19,8 @@
 //             (single CoT); 512-thread CTAs two per SM (large batches); a thread-block cluster of
 //             up to 8 CTAs per step sharing its history scan over DSMEM (online LAST rounds).
 //             Offline single-CoT launches FUSE the fill: each step's CTA gets its output offsets
-//             by a decoupled look-back over the preceding steps and writes its matches and pairs.
+//             by summing the published counts of all preceding steps (the whole CTA, one memory
+//             latency) and writes its matches and pairs.
 //             Otherwise the survivors are stashed and the last CTA scans the per-step counts.
 //   fill    : (when not fused) one CTA per current step: write matches, targets, target_off, pairs
 #include <cfloat>
@@ -57,9 +58,8 @@ struct CandWs {
   double* stash_cos;     // [match_cap]
   int32_t* stash_j;
   int2* gtab;            // [4*num_tokens] {key, count} global tables of oversize steps
-  int32_t* lb_flag;      // [step_cap] fused fill: 0 none, 1 aggregate, 2 inclusive prefix (zeroed by encode)
-  int4* lb_agg;          // [step_cap] {matches, targets, pairs} of the step
-  int4* lb_inc;          // [step_cap] inclusive prefix through the step
+  int4* lb_agg;          // [step_cap] fused fill: {matches+1, targets+1, pairs+1, 1} of the step, 0 = not yet
+                         // published (zeroed by encode)
 };
 
 CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_cap) {
@@ -78,9 +78,7 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   c.stash_cos = w.take<double>(match_cap + 1);
   c.stash_j = w.take<int32_t>(match_cap + 1);
   c.gtab = w.take<int2>(4 * num_tokens + 1);
-  c.lb_flag = w.take<int32_t>(step_cap + 1);
   c.lb_agg = w.take<int4>(step_cap + 1);
-  c.lb_inc = w.take<int4>(step_cap + 1);
   return c;
 }
 
@@ -194,7 +192,7 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
-    a.ws.lb_flag[g] = 0;                                  // stage1's look-back flags (fused fill)
+    a.ws.lb_agg[g] = make_int4(0, 0, 0, 0);               // stage1's published counts (fused fill)
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
@@ -274,7 +272,7 @@ __global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t G = total_steps(a);
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
-    a.ws.lb_flag[g] = 0;                                  // stage1's look-back flags (fused fill)
+    a.ws.lb_agg[g] = make_int4(0, 0, 0, 0);               // stage1's published counts (fused fill)
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
@@ -560,62 +558,55 @@ __device__ void scan_counts3(const CandArgs& a, int64_t G, int64_t* sh) {
   if (threadIdx.x == 0) { a.ws.off_m[G] = cm; a.ws.off_t[G] = ct; a.ws.off_p[G] = cp; }
 }
 
-__device__ __forceinline__ int32_t s1_ld_acquire(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ int4 s1_ld_relaxed(const int4* p) {
+  int4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
   return v;
 }
-__device__ __forceinline__ void s1_st_release(int32_t* p, int32_t v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void s1_st_relaxed(int4* p, int4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
-// Fused fill (offline, one CTA per step in one wave): step g publishes its {matches, targets,
-// pairs} counts and obtains the exclusive prefix over steps < g by a decoupled look-back (warp 0,
-// 32 predecessors per window; every step publishes its aggregate before it waits, and steps are
-// taken in ascending order by co-resident CTAs, so the waits always end). Returns the prefix to
-// every thread of the CTA.
-__device__ int4 s1_lookback(const CandArgs& a, int64_t g, int32_t m, int32_t t, int32_t p, int4* s_out) {
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
-    if (g == 0) {
-      if (lane == 0) {
-        a.ws.lb_inc[0] = make_int4(m, t, p, 0);
-        __threadfence();
-        s1_st_release(a.ws.lb_flag, 2);
-        *s_out = make_int4(0, 0, 0, 0);
-      }
-    } else {
-      if (lane == 0) {
-        a.ws.lb_agg[g] = make_int4(m, t, p, 0);
-        __threadfence();
-        s1_st_release(a.ws.lb_flag + g, 1);
-      }
-      int32_t rm = 0, rt = 0, rp = 0;
-      for (int64_t q0 = g - 1;; q0 -= 32) {
-        const int64_t q = q0 - lane;
-        int32_t f = 2;
-        if (q >= 0) {
-          while ((f = s1_ld_acquire(a.ws.lb_flag + q)) == 0) {
-          }
-        }
-        const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 32;           // nearest predecessor with a prefix
-        int4 v = make_int4(0, 0, 0, 0);
-        if (q >= 0 && lane < stop) v = __ldcg(a.ws.lb_agg + q);
-        else if (q >= 0 && lane == stop) v = __ldcg(a.ws.lb_inc + q);
-        if (lane > stop) v = make_int4(0, 0, 0, 0);
-        rm += warp_sum(v.x);
-        rt += warp_sum(v.y);
-        rp += warp_sum(v.z);
-        if (stop < 32) break;
-      }
-      if (lane == 0) {
-        a.ws.lb_inc[g] = make_int4(rm + m, rt + t, rp + p, 0);
-        __threadfence();
-        s1_st_release(a.ws.lb_flag + g, 2);
-        *s_out = make_int4(rm, rt, rp, 0);
-      }
-    }
+// Fused fill (offline, one CTA per step): step g publishes its {matches, targets, pairs} counts
+// and obtains the exclusive prefix over steps < g by summing the published counts of ALL its
+// predecessors with the whole CTA -- independent loads, one memory latency, where a look-back
+// walk through 32-step windows costs two dependent L2 round trips per window. Each count is
+// stored +1, so every 32-bit word is its own "published" flag (a zero word: not yet; no separate
+// flag, no fence ordering between two locations). Every step publishes before it waits and steps
+// are taken in ascending order by co-resident CTAs, so the waits always end. Returns the prefix
+// to every thread of the CTA.
+template <int NT>
+__device__ int4 s1_prefix(const CandArgs& a, int64_t g, int32_t m, int32_t t, int32_t p, int4* s_out) {
+  __shared__ int s_part[3][NT / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s1_st_relaxed(a.ws.lb_agg + g, make_int4(m + 1, t + 1, p + 1, 1));
+  int rm = 0, rt = 0, rp = 0;
+  for (int64_t q = threadIdx.x; q < g; q += NT) {
+    int4 v;
+    do {
+      v = s1_ld_relaxed(a.ws.lb_agg + q);
+    } while (v.x == 0 || v.y == 0 || v.z == 0);
+    rm += v.x - 1;
+    rt += v.y - 1;
+    rp += v.z - 1;
+  }
+  rm = warp_sum(rm);
+  rt = warp_sum(rt);
+  rp = warp_sum(rp);
+  if (lane == 0) { s_part[0][w] = rm; s_part[1][w] = rt; s_part[2][w] = rp; }
+  __syncthreads();
+  if (w == 0) {
+    int x = 0, y = 0, z = 0;
+    if (lane < NT / 32) { x = s_part[0][lane]; y = s_part[1][lane]; z = s_part[2][lane]; }
+    x = warp_sum(x);
+    y = warp_sum(y);
+    z = warp_sum(z);
+    if (lane == 0) *s_out = make_int4(x, y, z, 0);
   }
   __syncthreads();
   return *s_out;
@@ -677,11 +668,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
       if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
       if (fused) {
         if (g == G - 1) {
-          const int4 pre = s1_lookback(a, g, 0, 0, 0, &s_lb);
+          const int4 pre = s1_prefix<NT>(a, g, 0, 0, 0, &s_lb);
           s1_totals(a, pre);
         } else if (threadIdx.x == 0) {
-          if (g == 0) { a.ws.lb_inc[0] = make_int4(0, 0, 0, 0); __threadfence(); s1_st_release(a.ws.lb_flag, 2); }
-          else { a.ws.lb_agg[g] = make_int4(0, 0, 0, 0); __threadfence(); s1_st_release(a.ws.lb_flag + g, 1); }
+          s1_st_relaxed(a.ws.lb_agg + g, make_int4(1, 1, 1, 1));
         }
       }
       continue;
@@ -828,7 +818,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     __syncthreads();
     if (fused) {
       // offsets of this step's outputs, then the fill kernel's work done here
-      const int4 pre = s1_lookback(a, g, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
+      const int4 pre = s1_prefix<NT>(a, g, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
       if (g == G - 1) s1_totals(a, make_int4(pre.x + m, pre.y + (int32_t)sm.acc_t, pre.z + (int32_t)sm.acc_p, 0));
       const int64_t mo = pre.x, to = pre.y, po = pre.z;
       for (int r = threadIdx.x; r < m; r += kNTs) {
@@ -1092,7 +1082,7 @@ extern "C" memshare_status memshare_step_candidates(
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     // offline single-CoT shape (one 1024-thread CTA per step, no cluster): stage1 also writes the
-    // matches and pairs (look-back offsets), so no fill kernel and no last-CTA scan
+    // matches and pairs (offsets from the predecessors' published counts), so no fill kernel and no last-CTA scan
     a.fused = (cur_mode == MEMSHARE_CUR_ALL && !half && cs == 1 && fused_env()) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
