@@ -288,7 +288,7 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
     from paper_2507_21433_b200 import _lib as L
-    from paper_2507_21433_b200.pipeline import MemSharePath
+    from paper_2507_21433_b200.pipeline import MemSharePath, pack_inputs
 
     w = make_workload(args.config, args.seed, rank if args.mode == "seq" else 0, args.seqs_per_gpu, args.wave,
                       world if args.mode == "seq" else 1)
@@ -507,22 +507,21 @@ def main():
     # ---------------------------------------------------------------- e2e through the public API
     e2e = None
     if not args.no_e2e:
-        pin = lambda x: torch.as_tensor(np.ascontiguousarray(x)).pin_memory()
-        h_in = {"tokens": pin(b.tokens.astype(np.int32)), "seq_tok_off": pin(b.seq_tok_off.astype(np.int64)),
-                "gen_start": pin(b.gen_start.astype(np.int32)), "final": pin(b.final.astype(np.uint8)),
-                "state": pin(np.concatenate([np.asarray([w.free_count], np.int64).view(np.int32),
-                                             w.table.astype(np.int32).ravel(), w.refcount.astype(np.int32),
-                                             w.free_list.astype(np.int32)]))}
-        h2d = sum(x.numel() * x.element_size() for x in h_in.values())
-        out_dec = torch.empty(path.decisions.numel(), dtype=torch.uint8).pin_memory()
-        out_tab = torch.empty(path.table.shape, dtype=torch.int32).pin_memory()
-        out_cnt = torch.empty(5, dtype=torch.int64).pin_memory()
-        d2h = out_dec.numel() + out_tab.numel() * 4 + out_cnt.numel() * 8
-        cnt_dev = torch.empty(5, dtype=torch.int64, device=dev)
+        # one pinned upload of the round's inputs (trace + serving state, MemSharePath's layout) and
+        # one pinned read-back each of the outputs (counters + decisions) and the state head
+        # (free count + rewritten block table)
+        host_in, _ = pack_inputs(b.tokens, b.seq_tok_off, b.gen_start, b.final, w.table, w.refcount, w.free_list,
+                                 w.free_count)
+        h_in = torch.from_numpy(host_in).pin_memory()
+        assert h_in.numel() == path.inputs.numel()
+        h2d = h_in.numel() * 4
+        n_head = 2 + path.table.numel()
+        out_o = torch.empty(path.outputs.numel(), dtype=torch.uint8).pin_memory()
+        out_s = torch.empty(n_head, dtype=torch.int32).pin_memory()
+        d2h = out_o.numel() + out_s.numel() * 4
 
         def e2e_step():
-            for n, x in h_in.items():
-                getattr(path, n).copy_(x, non_blocking=True)
+            path.inputs.copy_(h_in, non_blocking=True)
             path.segment()
             path.candidates(w.tau_s)
             if args.mode == "headshard":
@@ -530,11 +529,8 @@ def main():
             else:
                 path.distance_call(w.tau_b)
             path.remap()
-            torch.cat([path.num_pairs, path.num_targets, path.num_freed, path.affected, path.free_count],
-                      out=cnt_dev)
-            out_dec.copy_(path.decisions, non_blocking=True)
-            out_tab.copy_(path.table, non_blocking=True)
-            out_cnt.copy_(cnt_dev, non_blocking=True)
+            out_o.copy_(path.outputs, non_blocking=True)
+            out_s.copy_(path.state[:n_head], non_blocking=True)
 
         e2e_body = e2e_step
         e2e_graph = not args.no_graph and collective == "none"
@@ -568,11 +564,12 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = float(te[0])
-        assert int(out_cnt[0]) == P
+        assert int(out_o[:64].view(torch.int64)[1]) == P
         e2e = {"value": pairs_all / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms, "steps": n_e2e,
-               "note": "public API (MemSharePath over the C ABI); per step: pinned H2D of tokens/offsets/table/"
-                       "refcounts/free list, the 4 calls, D2H of decisions/table/counters, stream sync; the KV pool "
+               "note": "public API (MemSharePath over the C ABI); per step: one pinned H2D of the round's inputs "
+                       "(tokens, offsets, block table, refcounts, free list), the 4 calls, D2H of counters + "
+                       "decisions and of the rewritten table, stream sync; the KV pool "
                        "is the device-resident serving cache" + ("; the round (H2D + calls + D2H) is replayed as one "
                        "CUDA graph captured through MemSharePath.capture, a host sync per step" if e2e_graph else
                        "; calls launched eagerly")}

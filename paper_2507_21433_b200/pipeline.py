@@ -33,8 +33,37 @@ def _dev_i32(a, dev):
     return torch.as_tensor(np.ascontiguousarray(a, np.int32), device=dev)
 
 
-def _dev_i64(a, dev):
-    return torch.as_tensor(np.ascontiguousarray(a, np.int64), device=dev)
+def pack_inputs(tokens, seq_tok_off, gen_start, final, table, refcount, free_list, free_count):
+    """Host int32 buffer holding one round's inputs in MemSharePath's layout, and the layout
+    (int32 offsets of each part). A serving loop fills a pinned copy of this and uploads it with a
+    single host-to-device copy into ``MemSharePath.inputs``."""
+    ns = int(len(gen_start))
+    tok = tokens if not isinstance(tokens, torch.Tensor) else None
+    nt_tok = int(len(tokens))
+    table = np.ascontiguousarray(table, np.int32)
+    refcount = np.ascontiguousarray(refcount, np.int32)
+    free_list = np.ascontiguousarray(free_list, np.int32)
+    lay = {"seq_tok_off": 0, "state": 2 * (ns + 1)}
+    n_state = 2 + table.size + refcount.size + free_list.size
+    lay["tokens"] = lay["state"] + n_state
+    lay["gen_start"] = lay["tokens"] + nt_tok
+    lay["final"] = lay["gen_start"] + ns
+    total = lay["final"] + (ns + 3) // 4
+    host = np.zeros(max(total, 1), np.int32)
+    host[:lay["state"]] = np.ascontiguousarray(seq_tok_off, np.int64).view(np.int32)
+    s0 = lay["state"]
+    host[s0:s0 + 2] = np.asarray([int(free_count)], np.int64).view(np.int32)
+    o = s0 + 2
+    for part in (table.ravel(), refcount, free_list):
+        host[o:o + part.size] = part
+        o += part.size
+    if tok is not None:
+        host[lay["tokens"]:lay["gen_start"]] = np.ascontiguousarray(tok, np.int32)
+    host[lay["gen_start"]:lay["final"]] = np.ascontiguousarray(gen_start, np.int32)
+    fin = np.zeros(((ns + 3) // 4) * 4, np.uint8)
+    fin[:ns] = np.ascontiguousarray(final, np.uint8)
+    host[lay["final"]:total] = fin.view(np.int32)
+    return host, lay
 
 
 class MemSharePath:
@@ -46,27 +75,28 @@ class MemSharePath:
         self.delims = np.ascontiguousarray(delim_ids, np.int32)
         self.num_seqs = int(len(gen_start))
         self.num_tokens = int(len(tokens))
-        self.tokens = _dev_i32(tokens, self.dev)
-        self.seq_tok_off = _dev_i64(seq_tok_off, self.dev)
-        self.gen_start = _dev_i32(gen_start, self.dev)
-        self.final = torch.as_tensor(np.ascontiguousarray(final, np.uint8), device=self.dev)
         table = np.ascontiguousarray(table, np.int32)
         self.table_stride = int(table.shape[1])
-        # the serving state remap() mutates, in ONE buffer (a single copy snapshots / restores it):
-        # [free_count int64][block table][refcounts][free list]
-        refcount = np.ascontiguousarray(refcount, np.int32)
-        free_list = np.ascontiguousarray(free_list, np.int32)
-        nt, nr, nf = table.size, refcount.size, free_list.size
-        host = np.zeros(2 + nt + nr + nf, np.int32)
-        host[:2] = np.asarray([int(free_count)], np.int64).view(np.int32)
-        host[2:2 + nt] = table.ravel()
-        host[2 + nt:2 + nt + nr] = refcount
-        host[2 + nt + nr:] = free_list
-        self.state = torch.as_tensor(host, device=self.dev)
-        self.free_count = self.state[:2].view(torch.int64)
-        self.table = self.state[2:2 + nt].view(table.shape)
-        self.refcount = self.state[2 + nt:2 + nt + nr]
-        self.free_list = self.state[2 + nt + nr:]
+        # Every per-round input in ONE int32 buffer (a serving loop uploads a round with one copy;
+        # the state remap() mutates is one contiguous sub-range, so one copy snapshots / restores it):
+        #   [seq_tok_off int64][free_count int64][block table][refcounts][free list][tokens][gen_start][final u8]
+        host, lay = pack_inputs(tokens, seq_tok_off, gen_start, final, table, refcount, free_list, free_count)
+        self.layout = lay
+        self.inputs = torch.as_tensor(host, device=self.dev)
+        if isinstance(tokens, torch.Tensor):         # e.g. a device-resident trace: copied in place
+            self.inputs[lay["tokens"]:lay["tokens"] + self.num_tokens].copy_(tokens.view(-1).to(torch.int32))
+        i = self.inputs
+        self.seq_tok_off = i[lay["seq_tok_off"]:lay["state"]].view(torch.int64)
+        self.state = i[lay["state"]:lay["tokens"]]
+        st = self.state
+        nt, nr = table.size, int(np.asarray(refcount).size)
+        self.free_count = st[:2].view(torch.int64)
+        self.table = st[2:2 + nt].view(table.shape)
+        self.refcount = st[2 + nt:2 + nt + nr]
+        self.free_list = st[2 + nt + nr:]
+        self.tokens = i[lay["tokens"]:lay["tokens"] + self.num_tokens]
+        self.gen_start = i[lay["gen_start"]:lay["gen_start"] + self.num_seqs]
+        self.final = i[lay["final"]:].view(torch.uint8)[:self.num_seqs]
         self.num_blocks = int(num_blocks)
         self.k_pool, self.v_pool = k_pool, v_pool
         self.pool = L.KVPool(k_pool.data_ptr() if k_pool is not None else None,
@@ -76,8 +106,6 @@ class MemSharePath:
         self.block_size = block_size
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         z64 = lambda: torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self.num_matches, self.num_pairs, self.num_targets = z64(), z64(), z64()
-        self.num_freed, self.affected = z64(), z64()
         self.seq_step_off = torch.zeros(self.num_seqs + 1, dtype=torch.int64, device=self.dev)
         self.partial_sq = None
         self.set_caps(caps or Caps(step=max(1, self.num_tokens), match=max(1024, self.num_tokens),
@@ -110,7 +138,13 @@ class MemSharePath:
         self.target_off = e(caps.target + 1, torch.int64)
         self.distance = e(caps.pair, torch.float32)
         self.under = e(caps.pair, torch.uint8)
-        self.decisions = e(caps.target * 32, torch.uint8)
+        # the per-round outputs a serving loop reads back, in ONE buffer (one copy):
+        #   [num_matches, num_pairs, num_targets, num_freed, affected, 3 spare: int64][decisions]
+        self.outputs = torch.zeros(64 + max(1, caps.target) * 32, dtype=torch.uint8, device=d)
+        self.counters = self.outputs[:64].view(torch.int64)
+        c = self.counters
+        self.num_matches, self.num_pairs, self.num_targets, self.num_freed, self.affected = (c[j:j + 1] for j in range(5))
+        self.decisions = self.outputs[64:]
         ws = max(L.segment_steps_workspace_size(self.num_tokens, self.num_seqs, caps.step),
                  L.step_candidates_workspace_size(self.num_tokens, self.num_seqs, caps.step, caps.match),
                  L.block_distance_workspace_size(self.dims, self.num_blocks, caps.pair, caps.target,
