@@ -298,9 +298,30 @@ __device__ __forceinline__ bool cand_before(double ca, int32_t ja, double cb, in
   return ca > cb || (ca == cb && ja < jb);
 }
 
-// bitonic sort of (cos desc, j asc) over n entries padded to a power of two
+// Short lists (n <= kRankSort and <= blockDim) are sorted by rank: each thread ranks its own entry
+// against all n (broadcast shared-memory reads) and scatters it -- two barriers, where the bitonic
+// network costs one barrier per stage (log2(n)(log2(n)+1)/2 stages). Keys are distinct (j is unique
+// among a step's candidates), so the ranks are a permutation.
+constexpr int kRankSort = 256;
+
+// sort of (cos desc, j asc) over n entries: by rank, else bitonic over n padded to a power of two
 __device__ void sort_cands(double* cs, int32_t* js, int n) {
   if (n <= 1) return;
+  if (n <= kRankSort && n <= (int)blockDim.x) {
+    const int i = threadIdx.x;
+    double c = 0.0;
+    int32_t j = 0;
+    int rank = 0;
+    if (i < n) {
+      c = cs[i];
+      j = js[i];
+      for (int k = 0; k < n; ++k) rank += cand_before(cs[k], js[k], c, j) ? 1 : 0;
+    }
+    __syncthreads();
+    if (i < n) { cs[rank] = c; js[rank] = j; }
+    __syncthreads();
+    return;
+  }
   const int np = (int)pow2_ceil((uint32_t)n);
   for (int i = n + threadIdx.x; i < np; i += blockDim.x) {
     cs[i] = -2.0;
@@ -325,8 +346,21 @@ __device__ void sort_cands(double* cs, int32_t* js, int n) {
   }
 }
 
-__device__ void sort_ints(int32_t* v, int n) {
+__device__ void sort_ints(int32_t* v, int n) {   // distinct values
   if (n <= 1) return;
+  if (n <= kRankSort && n <= (int)blockDim.x) {
+    const int i = threadIdx.x;
+    int32_t x = 0;
+    int rank = 0;
+    if (i < n) {
+      x = v[i];
+      for (int k = 0; k < n; ++k) rank += v[k] < x ? 1 : 0;
+    }
+    __syncthreads();
+    if (i < n) v[rank] = x;
+    __syncthreads();
+    return;
+  }
   const int np = (int)pow2_ceil((uint32_t)n);
   for (int i = n + threadIdx.x; i < np; i += blockDim.x) v[i] = INT_MAX;
   __syncthreads();
@@ -366,10 +400,23 @@ __device__ void prepare_cands(const CandArgs& a, Cands& c, int64_t gfirst) {
     c.flen[r] = hi > lo ? hi - lo : 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int r = 0; r < c.m; ++r) { c.cum[r] = acc; acc += c.flen[r]; }
-    c.cum[c.m] = acc;
+  if (a.pairing == MEMSHARE_PAIR_ALIGNED) return;     // only CROSS slots index through cum
+  if (threadIdx.x < 32) {                            // exclusive prefix of flen, one warp
+    const int lane = threadIdx.x;
+    int32_t carry = 0;
+    for (int base = 0; base < c.m; base += 32) {
+      const int r = base + lane;
+      const int32_t f = r < c.m ? c.flen[r] : 0;
+      int32_t v = f;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (r < c.m) c.cum[r] = carry + v - f;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) c.cum[c.m] = carry;
   }
   __syncthreads();
 }
@@ -400,17 +447,46 @@ __device__ int32_t target_sources(const CandArgs& a, const Cands& c, const int32
   const int lane = threadIdx.x & 31;
   const int32_t nslots = a.pairing == MEMSHARE_PAIR_ALIGNED ? c.m : c.cum[c.m];
   int32_t kept_total = 0;
+  // a slot is kept unless an earlier slot holds the same physical block: each lane's block is
+  // compared with the earlier slots' blocks broadcast from the lanes that loaded them (one table
+  // load per lane per 32-slot window instead of a per-lane walk over all earlier slots)
+  auto slot_phys = [&](int32_t e, bool& in_range) -> int32_t {
+    const int32_t lg = e < nslots ? slot_logical(c, a.pairing, i, e) : -1;
+    in_range = lg >= 0 && lg < a.table_stride;
+    return in_range ? trow[lg] : 0;
+  };
   for (int32_t eb = 0; eb < nslots; eb += 32) {
     const int32_t e = eb + lane;
-    int32_t lg = e < nslots ? slot_logical(c, a.pairing, i, e) : -1;
-    bool keep = lg >= 0;
-    int32_t ph = keep ? phys_of(a, trow, lg) : -1;
-    if (keep) {
-      for (int32_t e2 = 0; e2 < e; ++e2) {
-        const int32_t lg2 = slot_logical(c, a.pairing, i, e2);
-        if (lg2 >= 0 && lg2 < a.table_stride && trow[lg2] == ph) { keep = false; break; }
+    const int32_t lg = e < nslots ? slot_logical(c, a.pairing, i, e) : -1;
+    const int32_t ph = lg >= 0 ? phys_of(a, trow, lg) : -1;
+    bool dup = false;
+    for (int32_t pb = 0; pb < eb; pb += 32) {
+      bool r2;
+      const int32_t p2 = slot_phys(pb + lane, r2);
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const int32_t x = __shfl_sync(0xffffffffu, p2, t);
+        const bool rx = __shfl_sync(0xffffffffu, r2, t);
+        dup |= rx && x == ph;
       }
     }
+    bool r1;
+    const int32_t p1 = slot_phys(e, r1);
+    // within the window: lanes holding the same in-range block share a match mask (out-of-range
+    // lanes get a key of their own); a lane whose slot is out of range (ph = INT_MIN, corrupt
+    // table row) is compared lane by lane, as the earlier windows are
+    const unsigned long long key = r1 ? (unsigned long long)(uint32_t)p1 : (1ull << 32) | (unsigned)lane;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    dup |= (same & ((1u << lane) - 1u)) != 0u;
+    if (__any_sync(0xffffffffu, lg >= 0 && !r1)) {
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const int32_t x = __shfl_sync(0xffffffffu, p1, t);
+        const bool rx = __shfl_sync(0xffffffffu, r1, t);
+        dup |= t < lane && rx && x == ph;
+      }
+    }
+    const bool keep = lg >= 0 && !dup;
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (out != nullptr && keep) {
       const int64_t pos = out_pos + kept_total + __popc(bal & ((1u << lane) - 1u));
