@@ -15,6 +15,7 @@ timeout 1200 python scripts/sweep_c4.py --seqs 16 > gpurun_out/ev_sweep_c4.jsonl
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 60 --csv --log-file gpurun_out/ev_launches_c2.csv python bench.py --steps 10 --warmup 5 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:distance_st_kernel -s 4 -c 1 -o gpurun_out/ev_dist_c2 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ev_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:distance_st_kernel -s 3 -c 1 -o gpurun_out/ev_dist_c4 python bench.py --config c4 --seqs-per-gpu 16 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ev_ncu_c4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage1_kernel -s 4 -c 1 -o gpurun_out/ev_s1_c2 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ev_ncu_s1.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_split -s 2 -c 1 -o gpurun_out/ev_attn python scripts/bench_rows.py --rows f1 > gpurun_out/ev_ncu_attn.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ev_pytest.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.txt 2>&1

@@ -177,6 +177,51 @@ def test_bit_reproducible_rounds(cur_mode):
         assert np.array_equal(s0[k], s1[k]), k
 
 
+@pytest.mark.parametrize("pairing,tau_s", [(oracle.ALIGNED, 0.5), (oracle.CROSS, 0.3)])
+def test_second_round_on_shared_blocks(pairing, tau_s):
+    """A round on the state a previous round left: after the zero-copy remap
+    several logical blocks share one physical block, so a target's source slots repeat physical
+    blocks and only the first slot of each is kept (the dedup; R25, oracle_step_candidates). Round 2 is compared in
+    full with the oracle run on round 1's table, refcounts and free list; CROSS at a low tau_s gives
+    targets with more than 32 source slots (the dedup across 32-slot windows)."""
+    import torch
+    w = workloads.small(SMALL, 2, 2500, seed=11, eta=0.0)
+    p = make_path(w)
+    tau_b = 10.0 * w.tau_b                       # accept most targets: many shared blocks after round 1
+    p.autosize(tau_s, pairing=pairing, slack=1.0)
+    p.round(tau_s, tau_b, pairing=pairing)
+    torch.cuda.synchronize()
+    assert p.read_status() == 0
+    s1 = p.read_state()
+    assert s1["num_freed"] > 0 and (s1["refcount"] > 1).any()
+    p.round(tau_s, tau_b, pairing=pairing)      # round 2 on the remapped state
+    torch.cuda.synchronize()
+    assert p.read_status() == 0
+    st = oracle_steps(w)
+    assert_steps_equal(p.read_steps(), st)
+    oc = oracle_candidates(w, st, tau_s, 0, pairing, table=s1["table"])
+    assert_candidates_equal(p.read_candidates(), oc)
+    # the dedup did drop slots: the same matches on a table without shared blocks give more pairs
+    uniq = np.arange(s1["table"].size, dtype=np.int32).reshape(s1["table"].shape)
+    assert oracle_candidates(w, st, tau_s, 0, pairing, table=uniq)["pairs"]["seq"].size > oc["pairs"]["seq"].size
+    if pairing == oracle.CROSS:
+        assert np.diff(oc["target_off"]).max() > 0
+    kh, vh = host_pool_from_device(p.k_pool, p.v_pool)
+    sh = w.shape
+    pr = oc["pairs"]
+    D = oracle.block_distance(kh, vh, p.pool.layer_stride, p.pool.block_stride, sh.num_layers, sh.num_kv_heads,
+                              sh.num_kv_heads, sh.head_dim, sh.block_size, pr["target_phys"], pr["source_phys"])
+    gd = p.read_distance()
+    compare_distances(gd["distance"], D)
+    compare_decisions(gd["decisions"], D, oc["target_off"], pr["source_logical"], tau_b)
+    s2 = p.read_state()
+    st_o, tab, rc, fl, fc, nf, af = oracle.remap(s1["table"], s1["refcount"], s1["free_list"], s1["free_count"],
+                                                 gd["decisions"], sh.block_size)
+    assert st_o == 0
+    assert np.array_equal(s2["table"], tab) and np.array_equal(s2["refcount"], rc)
+    assert np.array_equal(s2["free_list"], fl) and s2["free_count"] == fc and s2["num_freed"] == nf
+
+
 def test_degenerate_rounds():
     """Rounds with nothing to share: tau_s = 1.0 (strict 'exceeding' can never hold) gives no
     match, no pair, no target -- the distance call and the remap are no-ops and the table,
