@@ -187,7 +187,7 @@ def test_second_round_on_shared_blocks(pairing, tau_s):
     import torch
     w = workloads.small(SMALL, 2, 2500, seed=11, eta=0.0)
     p = make_path(w)
-    tau_b = 10.0 * w.tau_b                       # accept most targets: many shared blocks after round 1
+    tau_b = 1e-3                                 # eta = 0: planted copies are exact (D = 0), all accepted
     p.autosize(tau_s, pairing=pairing, slack=1.0)
     p.round(tau_s, tau_b, pairing=pairing)
     torch.cuda.synchronize()
@@ -203,9 +203,10 @@ def test_second_round_on_shared_blocks(pairing, tau_s):
     assert_candidates_equal(p.read_candidates(), oc)
     # the dedup did drop slots: the same matches on a table without shared blocks give more pairs
     uniq = np.arange(s1["table"].size, dtype=np.int32).reshape(s1["table"].shape)
-    assert oracle_candidates(w, st, tau_s, 0, pairing, table=uniq)["pairs"]["seq"].size > oc["pairs"]["seq"].size
-    if pairing == oracle.CROSS:
-        assert np.diff(oc["target_off"]).max() > 0
+    ou = oracle_candidates(w, st, tau_s, 0, pairing, table=uniq)
+    assert ou["pairs"]["seq"].size > oc["pairs"]["seq"].size
+    if pairing == oracle.CROSS:                  # targets with more than 32 source slots
+        assert np.diff(ou["target_off"]).max() > 32
     kh, vh = host_pool_from_device(p.k_pool, p.v_pool)
     sh = w.shape
     pr = oc["pairs"]
