@@ -113,7 +113,8 @@ struct CandArgs {
   int64_t* num_targets;
   int32_t* status;
   int32_t fused;        // offline single-CoT launch: stage1 writes matches / pairs itself (no fill kernel)
-  int32_t dbg_skip;     // tuning only (env MEMSHARE_DEBUG_SKIP): bit0 history stream, bit1 pair count, bit2 last-CTA scan
+  int32_t dbg_skip;     // tuning only (env MEMSHARE_DEBUG_SKIP): bit3 phase stamps; in -DMEMSHARE_TUNING builds also
+                        // bit0 skip history stream, bit1 pair count, bit2 last-CTA scan, bit4 table probes
   CandWs ws;
 };
 
@@ -1094,7 +1095,13 @@ extern "C" memshare_status memshare_step_candidates(
   a.status = device_status;
   {
     static int dbg = -1;
-    if (dbg < 0) { const char* e = getenv("MEMSHARE_DEBUG_SKIP"); dbg = e ? atoi(e) : 0; }
+    if (dbg < 0) {
+      const char* e = getenv("MEMSHARE_DEBUG_SKIP");
+      dbg = e ? atoi(e) : 0;
+#ifndef MEMSHARE_TUNING
+      dbg &= 8;   // shipped library: only the (harmless) phase stamps; work-skipping masks need -DMEMSHARE_TUNING
+#endif
+    }
     a.dbg_skip = dbg;
   }
   Ws w{static_cast<char*>(workspace), 0};
