@@ -530,6 +530,20 @@ def test_c2_full_size_parity():
           f"near_tie={near_tie}")
 
 
+@pytest.mark.parametrize("length", [40000, 100000])
+def test_single_cot_more_steps_than_sms(length):
+    """The fused single-CoT Stage-1 shape with more finished steps than CTAs (a 40k / 100k-token
+    trace: ~400 / ~1,000 steps on 148 CTAs, each CTA taking several steps in ascending order):
+    every step's output offsets come from its predecessors' published counts, so the matches,
+    pairs and target offsets must still be bit-exact, and the history staging takes several
+    passes for the late steps."""
+    w = workloads.small(SMALL, 1, length, seed=21)
+    st = oracle_steps(w)
+    assert st["seq_step_off"][-1] > 2 * 148
+    p, oc, D, _ = full_parity(w)
+    assert oc["pairs"]["seq"].size > 0
+
+
 def test_c2_full_size_online_round():
     """configs[1] online: only the last finished step is current; Stage 1 runs as an
     8-CTA cluster over its 12k-token history; everything bit-exact / within tolerance."""
