@@ -185,6 +185,12 @@ __device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {
   return lo;
 }
 
+// publication keys of the fused fill: steps (offline) or sequences (online LAST rounds)
+__device__ __forceinline__ int64_t fill_keys(const CandArgs& a, int64_t G) {
+  const int64_t z = a.cur_mode == MEMSHARE_CUR_LAST ? (int64_t)a.num_seqs : G;
+  return z < a.step_cap + 1 ? z : a.step_cap + 1;
+}
+
 // One CTA per step (latency-optimal when the steps fit in one wave: a single CoT).
 __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   pdl_trigger();
@@ -192,7 +198,8 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   extern __shared__ int2 s_tab[];                         // [kSmemSlots]
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
+  const int64_t Z = fill_keys(a, G);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Z; g += (int64_t)gridDim.x * blockDim.x)
     a.ws.lb_agg[g] = make_int4(0, 0, 0, 0);               // stage1's published counts (fused fill)
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
@@ -272,7 +279,8 @@ __global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
   extern __shared__ int2 s_tab[];                         // [kSmemSlots] = kNW warps x kEncSlots
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t G = total_steps(a);
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x)
+  const int64_t Z = fill_keys(a, G);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Z; g += (int64_t)gridDim.x * blockDim.x)
     a.ws.lb_agg[g] = make_int4(0, 0, 0, 0);               // stage1's published counts (fused fill)
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
@@ -718,21 +726,34 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   DBG_T(0);
   const int64_t G = total_steps(a);
   __shared__ int4 s_lb;
-  if (fused && G == 0 && blockIdx.x == 0) s1_totals(a, make_int4(0, 0, 0, 0));
-  // LAST (online): the work list is one step per sequence, found directly; the counts of every
-  // other step are zeroed up front by all threads (one parallel pass instead of a chain of
-  // dependent loads per skipped step).
+  // LAST (online): the work list is one step per sequence, found directly; without the fused fill
+  // the counts of every other step are zeroed up front by all threads (one parallel pass instead
+  // of a chain of dependent loads per skipped step) for the last-CTA scan.
   const bool last_mode = a.cur_mode == MEMSHARE_CUR_LAST;
-  if (last_mode) {
+  const int64_t nwork = last_mode ? a.num_seqs : G;
+  // fused fill: work item wi publishes its counts at key wi (= g offline, = the sequence online);
+  // the last key also writes the totals
+  if (fused && nwork == 0 && blockIdx.x == 0) s1_totals(a, make_int4(0, 0, 0, 0));
+  auto publish_nothing = [&](int64_t key) {     // a work item without outputs (all CTA threads call it)
+    if (key == nwork - 1) {
+      const int4 pre = s1_prefix(a, key, 0, 0, 0, &s_lb);
+      s1_totals(a, pre);
+    } else if (threadIdx.x == 0) {
+      s1_st_relaxed(a.ws.lb_agg + key, make_int4(1, 1, 1, 1));
+    }
+  };
+  if (last_mode && !fused) {
     for (int64_t g = (int64_t)blockIdx.x * kNTs + threadIdx.x; g < G; g += (int64_t)gridDim.x * kNTs) {
       const int32_t s = a.ws.step_seq[g];
       if (g != a.seq_step_off[s + 1] - 1) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
     }
   }
-  const int64_t nwork = last_mode ? a.num_seqs : G;
   for (int64_t wi = cid; wi < nwork; wi += ncl) {
     const int64_t g = last_mode ? a.seq_step_off[wi + 1] - 1 : wi;
-    if (last_mode && (g < a.seq_step_off[wi] || g >= G)) continue;   // sequence without steps
+    if (last_mode && (g < a.seq_step_off[wi] || g >= G)) {            // sequence without steps
+      if (fused && crank == 0) publish_nothing(wi);
+      continue;
+    }
     const int32_t s = a.ws.step_seq[g];
     const int64_t gfirst = a.seq_step_off[s];
     const int64_t S = a.seq_step_off[s + 1] - gfirst;
@@ -740,14 +761,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     const int32_t nbag = a.step_nbag[g];
     if (nbag == 0 || !is_current(a, s, k, S)) {
       if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
-      if (fused) {
-        if (g == G - 1) {
-          const int4 pre = s1_prefix(a, g, 0, 0, 0, &s_lb);
-          s1_totals(a, pre);
-        } else if (threadIdx.x == 0) {
-          s1_st_relaxed(a.ws.lb_agg + g, make_int4(1, 1, 1, 1));
-        }
-      }
+      if (fused && crank == 0) publish_nothing(wi);
       continue;
     }
     const int64_t tok_base = a.seq_tok_off[s];
@@ -892,9 +906,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     __syncthreads();
     if (fused) {
       // offsets of this step's outputs, then the fill kernel's work done here
-      const int4 pre = s1_prefix(a, g, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
+      const int4 pre = s1_prefix(a, wi, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
       DBG_T(8);
-      if (g == G - 1) s1_totals(a, make_int4(pre.x + m, pre.y + (int32_t)sm.acc_t, pre.z + (int32_t)sm.acc_p, 0));
+      if (wi == nwork - 1) s1_totals(a, make_int4(pre.x + m, pre.y + (int32_t)sm.acc_t, pre.z + (int32_t)sm.acc_p, 0));
       const int64_t mo = pre.x, to = pre.y, po = pre.z;
       for (int r = threadIdx.x; r < m; r += kNTs) {
         if (mo + r < a.match_cap) {
@@ -1165,7 +1179,10 @@ extern "C" memshare_status memshare_step_candidates(
     cfg.numAttrs = 2;
     // offline single-CoT shape (one 1024-thread CTA per step, no cluster): stage1 also writes the
     // matches and pairs (offsets from the predecessors' published counts), so no fill kernel and no last-CTA scan
-    a.fused = (cur_mode == MEMSHARE_CUR_ALL && !half && cs == 1 && fused_env()) ? 1 : 0;
+    // (online LAST rounds fuse too: the keys are the sequences, one current step each)
+    a.fused = (!half && fused_env() &&
+               ((cur_mode == MEMSHARE_CUR_ALL && cs == 1) ||
+                (cur_mode == MEMSHARE_CUR_LAST && (int64_t)num_seqs <= step_cap + 1))) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
   }
