@@ -15,12 +15,13 @@
 //   encode  : n2 = sum count^2 per step (history norms) -- one CTA per step for a single CoT,
 //             one warp per step for large batches
 //   stage1  : per current step: table, streamed history dots, strict threshold, (cos desc, j asc)
-//             bitonic sort, top-K, count targets/pairs. Shapes: one 1024-thread CTA per step
-//             (single CoT); 512-thread CTAs two per SM (large batches); a thread-block cluster of
-//             up to 8 CTAs per step sharing its history scan over DSMEM (online LAST rounds).
-//             Offline single-CoT launches FUSE the fill: each step's CTA gets its output offsets
-//             by summing the published counts of all preceding steps (the whole CTA, one memory
-//             latency) and writes its matches and pairs.
+//             sort (by rank for <= 256 survivors, else bitonic), top-K, count targets/pairs.
+//             Shapes: one 1024-thread CTA per step (single CoT); 512-thread CTAs two per SM (large
+//             batches); a thread-block cluster of up to 8 CTAs per step sharing its history scan
+//             over DSMEM (online LAST rounds).
+//             Offline single-CoT launches and online LAST rounds FUSE the fill: each work item
+//             (step / sequence) gets its output offsets by summing the published counts of all
+//             preceding items (one warp, one memory latency) and writes its matches and pairs.
 //             Otherwise the survivors are stashed and the last CTA scans the per-step counts.
 //   fill    : (when not fused) one CTA per current step: write matches, targets, target_off, pairs
 #include <cfloat>
