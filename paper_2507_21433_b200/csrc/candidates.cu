@@ -19,10 +19,10 @@
 //             Shapes: one 1024-thread CTA per step (single CoT); 512-thread CTAs two per SM (large
 //             batches); a thread-block cluster of up to 8 CTAs per step sharing its history scan
 //             over DSMEM (online LAST rounds).
-//             Offline single-CoT launches and online LAST rounds FUSE the fill: each work item
+//             Offline single-CoT launches and online rounds FUSE the fill: each work item
 //             (step / sequence) gets its output offsets by summing the published counts of all
 //             preceding items (one warp, one memory latency) and writes its matches and pairs.
-//             Otherwise the survivors are stashed and the last CTA scans the per-step counts.
+//             The 512-thread batch shape stashes the survivors and its last CTA scans the counts.
 //   fill    : (when not fused) one CTA per current step: write matches, targets, target_off, pairs
 #include <cfloat>
 #include <climits>
@@ -1180,9 +1180,10 @@ extern "C" memshare_status memshare_step_candidates(
     cfg.numAttrs = 2;
     // offline single-CoT shape (one 1024-thread CTA per step, no cluster): stage1 also writes the
     // matches and pairs (offsets from the predecessors' published counts), so no fill kernel and no last-CTA scan
-    // (online LAST rounds fuse too: the keys are the sequences, one current step each)
+    // (online rounds fuse too: RANGE with the steps as keys -- the non-current ones publish
+    // zeros -- and LAST with the sequences as keys, one current step each)
     a.fused = (!half && fused_env() &&
-               ((cur_mode == MEMSHARE_CUR_ALL && cs == 1) ||
+               ((cur_mode != MEMSHARE_CUR_LAST && cs == 1) ||
                 (cur_mode == MEMSHARE_CUR_LAST && (int64_t)num_seqs <= step_cap + 1))) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
