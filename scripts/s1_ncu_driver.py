@@ -1,3 +1,4 @@
+"""ncu driver (tuning): a few segment + candidates calls on c2, for `ncu -k regex:stage1 ...`."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch
