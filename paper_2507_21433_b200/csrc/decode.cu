@@ -40,8 +40,10 @@ __global__ void __launch_bounds__(kAppNT) append_alloc_kernel(int32_t* table, in
                                                               int32_t* refcount, int32_t num_blocks,
                                                               const int32_t* free_list, int64_t* free_count,
                                                               int32_t block_size, AppWs ws, int32_t* status) {
-  pdl_trigger();
+  // wait first, then let the copy kernel launch: it reads the new rows before its own wait, so
+  // everything earlier on the stream (whoever wrote new_k / new_v) must be complete by then
   pdl_wait();
+  pdl_trigger();
   __shared__ int64_t sh[kAppNT / 32 + 1];
   const int64_t fc = *free_count;
   int err = 0;          // 2 capacity, 3 corruption, 1 invalid
@@ -113,19 +115,49 @@ __global__ void __launch_bounds__(kAppNT) append_alloc_kernel(int32_t* table, in
 
 // Copy the new K/V rows (h * d_h bf16 each, one per (layer, sequence)) into their slots. A warp
 // moves one row per iteration (16-byte vectors, K and V loads issued together, 32-bit index
-// math: the row index is split once per row, not per vector).
+// math: the row index is split once per row, not per vector). The first row of each warp is
+// loaded BEFORE the grid-dependency wait (the new rows are inputs, not written by the alloc
+// kernel), so those HBM reads overlap the allocation; only the destination waits for it.
 __global__ void __launch_bounds__(256) append_copy_kernel(uint16_t* k, uint16_t* v, int64_t layer_stride,
                                                           int64_t block_stride, int32_t num_layers, int32_t num_seqs,
                                                           int32_t row_elems, const uint16_t* new_k,
                                                           const uint16_t* new_v, AppWs ws) {
+  constexpr int kPre = 4;                        // 16-byte vectors per lane preloaded (rows <= 2 KiB per K|V)
   pdl_trigger();
-  pdl_wait();
-  if (__ldcg(ws.ok) == 0) return;
   const int lane = threadIdx.x & 31;
   const int32_t vec = row_elems / 8;             // 16-byte vectors per row
   const int32_t rows = num_layers * num_seqs;
   const int32_t warps = (int32_t)(gridDim.x * (blockDim.x / 32));
-  for (int32_t r = (int32_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)); r < rows; r += warps) {
+  const int32_t r0 = (int32_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5));
+  uint4 pk[kPre], pv[kPre];
+  const bool pre = r0 < rows && vec <= 32 * kPre;
+  if (pre) {
+    const uint4* sk = reinterpret_cast<const uint4*>(new_k + (int64_t)r0 * row_elems);
+    const uint4* sv = reinterpret_cast<const uint4*>(new_v + (int64_t)r0 * row_elems);
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      const int32_t c = lane + 32 * i;
+      if (c < vec) { pk[i] = __ldg(sk + c); pv[i] = __ldg(sv + c); }
+    }
+  }
+  pdl_wait();
+  if (__ldcg(ws.ok) == 0) return;
+  if (pre) {
+    const int32_t l = r0 / num_seqs, s = r0 - l * num_seqs;
+    const int32_t b = __ldcg(ws.slot_blk + s);
+    if (b >= 0) {
+      const int64_t dst = (int64_t)l * layer_stride + (int64_t)b * block_stride +
+                          (int64_t)__ldcg(ws.slot_off + s) * row_elems;
+      uint4* dk = reinterpret_cast<uint4*>(k + dst);
+      uint4* dv = reinterpret_cast<uint4*>(v + dst);
+#pragma unroll
+      for (int i = 0; i < kPre; ++i) {
+        const int32_t c = lane + 32 * i;
+        if (c < vec) { dk[c] = pk[i]; dv[c] = pv[i]; }
+      }
+    }
+  }
+  for (int32_t r = pre ? r0 + warps : r0; r < rows; r += warps) {
     const int32_t l = r / num_seqs, s = r - l * num_seqs;
     const int32_t b = __ldcg(ws.slot_blk + s);
     if (b < 0) continue;
