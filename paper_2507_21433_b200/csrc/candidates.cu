@@ -142,8 +142,15 @@ struct Table {
   bool global;
 };
 
+// Presence filter of a step's tokens for the history stream: 2^16 bits indexed by the top 16 bits
+// of the same multiplicative hash; a clear bit is a definite miss, so the stream skips the table
+// probe (and its divergent probe loop) for the history tokens the step does not contain.
+constexpr int kBmWords = 2048;
+static_assert(kBmWords == 2 * kCandCap, "the filter overlays jasc + flo");
+__device__ __forceinline__ uint32_t bm_bit(int32_t tok) { return ((uint32_t)tok * 0x9E3779B1u) >> 16; }
+
 __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, int64_t tok_base, int32_t start,
-                             int32_t end, int32_t nbag, int32_t smem_slots = kSmemSlots) {
+                             int32_t end, int32_t nbag, int32_t smem_slots = kSmemSlots, uint32_t* bm = nullptr) {
   Table tb;
   uint32_t cap;
   if (nbag <= smem_slots / 4) {
@@ -158,10 +165,16 @@ __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, i
   tb.mask = cap - 1;
   tb.shift = 32u - (31u - __clz(cap));
   for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) tb.slots[i] = make_int2(kEmpty, 0);
+  if (bm != nullptr)
+    for (int i = threadIdx.x; i < kBmWords; i += blockDim.x) bm[i] = 0u;
   __syncthreads();
   for (int32_t p = start + threadIdx.x; p < end; p += blockDim.x) {
     const int32_t tok = t[p];
     if (is_delim(tok, a.dl)) continue;
+    if (bm != nullptr) {
+      const uint32_t hb = bm_bit(tok);
+      atomicOr(bm + (hb >> 5), 1u << (hb & 31));
+    }
     uint32_t slot = hash_slot(tok, tb.shift);
     for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
       int* key = &tb.slots[slot].x;
@@ -547,8 +560,13 @@ struct SelSmem {
   int2 tab[S1Cfg<NT>::kSlots];
   double cs[kCandCap];
   int32_t js[kCandCap];
-  int32_t jasc[kCandCap];
-  int32_t flo[kCandCap];
+  union {                                     // the presence filter lives only during the history
+    struct {                                  // stream; jasc / flo only after it
+      int32_t jasc[kCandCap];
+      int32_t flo[kCandCap];
+    } l;
+    uint32_t bm[kBmWords];
+  } u;
   int32_t flen[kCandCap];
   int32_t cum[kCandCap + 1];
   int32_t hst[kChunk];
@@ -568,7 +586,8 @@ struct SelSmem {
 // adds its partial dot once per step it touches. A rolled loop on purpose: this code runs once
 // per launch, so instruction-fetch misses of an unrolled body cost more than the work.
 template <bool kGlobal>
-__device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, uint32_t shift, uint32_t* dot_lo,
+__device__ __forceinline__ void stream_history(const int2* tab, const uint32_t* bm, uint32_t mask, uint32_t shift,
+                                               uint32_t* dot_lo,
                                                uint32_t* dot_hi, const int32_t* hen, int32_t nj, int32_t d0,
                                                int32_t dn, const Delims& dl, const int32_t* s_tok, int32_t clo,
                                                int32_t chi, bool dbg_noprobe) {
@@ -594,6 +613,8 @@ __device__ __forceinline__ void stream_history(const int2* tab, uint32_t mask, u
     }
     if (tok == d0 || (dn > 1 && is_delim(tok, dl))) continue;
     if (dbg_noprobe) { acc += (uint32_t)(tok & 1); continue; }
+    const uint32_t hb = bm_bit(tok);
+    if (!((bm[hb >> 5] >> (hb & 31)) & 1u)) continue;   // not in the step: no probe
     uint32_t slot = hash_slot(tok, shift);
     int32_t c = 0;
 #pragma unroll 1
@@ -767,7 +788,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     }
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t* t = a.tokens + tok_base;
-    const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots);
+    const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots,
+                                 sm.u.bm);
     DBG_T(1);
     const double n2k = (double)a.ws.n2[g];
     if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
@@ -801,10 +823,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
         if (jb == 0 && clo == lo) DBG_T(14);
         if (!(a.dbg_skip & 1)) {
           if (tb.global)
-            stream_history<true>(tb.slots, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
+            stream_history<true>(tb.slots, sm.u.bm, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
                                  a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
           else
-            stream_history<false>(sm.tab, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
+            stream_history<false>(sm.tab, sm.u.bm, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
                                   a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
         }
         __syncthreads();
@@ -870,13 +892,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     const int64_t base = (int64_t)s_base;
     for (int r = threadIdx.x; r < m; r += kNTs) {
       if (!fused && base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
-      sm.jasc[r] = sm.js[r];
+      sm.u.l.jasc[r] = sm.js[r];
     }
     if (threadIdx.x == 0) { sm.acc_t = 0u; sm.acc_p = 0u; }
     __syncthreads();
     // a4: count targets and deduplicated pairs of this step
     DBG_T(4);
-    Cands c{m, sm.jasc, sm.flo, sm.flen, sm.cum};
+    Cands c{m, sm.u.l.jasc, sm.u.l.flo, sm.flen, sm.cum};
     prepare_cands(a, c, gfirst);
     DBG_T(5);
     const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
@@ -964,8 +986,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
 struct FillSmem {
   double cs[kCandCap];
   int32_t js[kCandCap];
-  int32_t jasc[kCandCap];
-  int32_t flo[kCandCap];
+  union {                                     // the presence filter lives only during the history
+    struct {                                  // stream; jasc / flo only after it
+      int32_t jasc[kCandCap];
+      int32_t flo[kCandCap];
+    } l;
+    uint32_t bm[kBmWords];
+  } u;
   int32_t flen[kCandCap];
   int32_t cum[kCandCap + 1];
   int32_t tc[kMaxTgt];
@@ -993,7 +1020,7 @@ __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
     for (int r = threadIdx.x; r < m; r += kNT) {
       const double cs = a.ws.stash_cos[sbase + r];
       const int32_t j = a.ws.stash_j[sbase + r];
-      sm.jasc[r] = j;
+      sm.u.l.jasc[r] = j;
       if (mo + r < a.match_cap) {
         memshare_step_match mt;
         mt.seq = s; mt.step = (int32_t)k; mt.cand_step = j; mt.rank = r; mt.cosine = cs;
@@ -1001,7 +1028,7 @@ __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
       }
     }
     __syncthreads();
-    Cands c{m, sm.jasc, sm.flo, sm.flen, sm.cum};
+    Cands c{m, sm.u.l.jasc, sm.u.l.flo, sm.flen, sm.cum};
     prepare_cands(a, c, gfirst);
     const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
     int32_t nt = fk_hi > fk_lo ? fk_hi - fk_lo : 0;
