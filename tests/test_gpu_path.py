@@ -544,6 +544,27 @@ def test_single_cot_more_steps_than_sms(length):
     assert oc["pairs"]["seq"].size > 0
 
 
+@pytest.mark.parametrize("empty_seq", [0, 2])
+def test_online_rounds_with_a_stepless_sequence(empty_seq):
+    """Online rounds (LAST and RANGE, fused fill) when one sequence has no finished step (no
+    delimiter, not final): its work item publishes zero counts -- as the first key, or as the
+    last key that also writes the totals -- and the other sequences' outputs are unchanged."""
+    import dataclasses
+    w = workloads.small(SMALL, 3, 2000, seed=13)
+    b = w.batch
+    toks = b.tokens.copy()
+    lo, hi = int(b.seq_tok_off[empty_seq]), int(b.seq_tok_off[empty_seq + 1])
+    seg = toks[lo:hi]
+    seg[np.isin(seg, b.delim_ids)] = 7                    # no delimiter left in that sequence
+    fin = np.asarray(b.final, np.uint8).copy()
+    fin[empty_seq] = 0                                    # and it is not final: no finished step
+    w2 = dataclasses.replace(w, batch=dataclasses.replace(b, tokens=toks, final=fin))
+    st = oracle_steps(w2)
+    assert st["seq_step_off"][empty_seq + 1] == st["seq_step_off"][empty_seq]
+    full_parity(w2, tau_s=0.5, cur_mode=oracle.CUR_LAST)
+    full_parity(w2, tau_s=0.5, cur_mode=oracle.CUR_RANGE, cb=[0, 1, 2], ce=[4, 6, 9])
+
+
 def test_c2_full_size_online_round():
     """configs[1] online: only the last finished step is current; Stage 1 runs as an
     8-CTA cluster over its 12k-token history; everything bit-exact / within tolerance."""
