@@ -1176,11 +1176,11 @@ extern "C" memshare_status memshare_step_candidates(
   {
     // cluster size per current step: online rounds (LAST: one current step per sequence) split
     // each step's history over up to 8 CTAs while the clusters still fit in one wave; offline
-    // (ALL) and RANGE calls keep one CTA per step. MEMSHARE_S1_CLUSTER overrides (tuning).
+    // (ALL) and RANGE calls keep one CTA per step. MEMSHARE_S1_CLUSTER overrides the LAST size (tuning).
     static int env_cs = -1;
     if (env_cs < 0) { const char* e = getenv("MEMSHARE_S1_CLUSTER"); env_cs = e ? atoi(e) : 0; }
     int cs = 1;
-    if (env_cs > 0) cs = env_cs;
+    if (env_cs > 0 && cur_mode == MEMSHARE_CUR_LAST) cs = env_cs;   // clusters only where tested: LAST rounds
     else if (cur_mode == MEMSHARE_CUR_LAST)
       for (int c = 8; c > 1; c >>= 1)
         if ((int64_t)num_seqs * c <= sms) { cs = c; break; }
