@@ -24,7 +24,7 @@ namespace {
 #define MS_SEG_NT 1024
 #endif
 #ifndef MS_SEG_ITEMS
-#define MS_SEG_ITEMS 4
+#define MS_SEG_ITEMS 2
 #endif
 constexpr int kNT = MS_SEG_NT;           // threads per tile
 constexpr int kItems = MS_SEG_ITEMS;     // tokens per thread (a 32-bit flag word each)
