@@ -499,6 +499,15 @@ __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
 // Finalisation: one CTA per target (grid-stride). FULL/PARTIAL read the per-warp partials the
 // streaming kernel left in the workspace (kernel boundary = the only synchronisation needed);
 // FINALIZE reads partial squared sums already reduced across ranks.
+// Zeroes the work ticket. A kernel rather than a memset node so the launch chain keeps its
+// programmatic dependent launches (the streaming kernel's CTAs wait for this grid to complete
+// before they take tickets).
+__global__ void ticket_reset_kernel(unsigned int* ticket) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
 __global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int from_partial) {
   pdl_trigger();
   pdl_wait();
@@ -663,7 +672,7 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
     launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 1);
     return launch_status();
   }
-  if (cudaMemsetAsync(a.ws.ticket, 0, sizeof(unsigned int), st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
+  launch_pdl(ticket_reset_kernel, dim3(1), dim3(32), 0, st, a.ws.ticket);
   const bool prof = g_prof_begin != nullptr && g_prof_end != nullptr;
   if (prof && cudaEventRecord(g_prof_begin, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   const bool partial = slice_bytes % ((int64_t)kre * kChunkUnit) != 0;
