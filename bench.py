@@ -37,8 +37,8 @@ UNIT = "pairs/s"
 # round over a single CoT-sized batch: <= 100 x 8 x SMs tokens, no cluster; MEMSHARE_FUSED_FILL=0 disables)
 def gpu_launches_per_step(num_tokens, sms=148):
     fused = num_tokens <= 100 * 8 * sms and os.environ.get("MEMSHARE_FUSED_FILL", "1") != "0"
-    # seg, encode, stage1, (fill), ticket reset, distance, finalize, remap
-    return 7 if fused else 8
+    # flag reset, seg, encode, stage1, (fill), ticket reset, distance, finalize, remap
+    return 8 if fused else 9
 
 
 def parse():

@@ -314,10 +314,18 @@ __global__ void __launch_bounds__(kNT, 1) seg_kernel(SegArgs a) {
   }
 }
 
+// zeroes the look-back flags (a kernel, not a memset node: keeps the launch chain programmatic)
+__global__ void flag_reset_kernel(int32_t* flag, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) flag[i] = 0;
+}
+
 }  // namespace
 }  // namespace ms
 
 using namespace ms;
+
 
 extern "C" size_t memshare_segment_steps_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap) {
   if (num_tokens < 0 || num_seqs < 0 || step_cap < 0) return 0;
@@ -352,8 +360,9 @@ extern "C" memshare_status memshare_segment_steps(const int32_t* tokens, int64_t
   a.ws = seg_layout(w, num_tokens);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t tiles = (num_tokens + kTile - 1) / kTile;
-  if (tiles > 0 && cudaMemsetAsync(a.ws.flag, 0, (size_t)tiles * sizeof(int32_t), st) != cudaSuccess)
-    return MEMSHARE_ERR_CUDA;
+  // the look-back flags are zeroed by a small kernel, not a memset node: it keeps the launch chain
+  // programmatic (seg_kernel's CTAs wait for it to complete before they publish)
+  if (tiles > 0) launch_pdl(flag_reset_kernel, dim3(1), dim3(256), 0, st, a.ws.flag, tiles);
   launch_pdl(seg_kernel, dim3((unsigned)(tiles < 1 ? 1 : tiles)), dim3(kNT), 0, st, a);
   return launch_status();
 }
