@@ -47,6 +47,7 @@ constexpr int32_t kEmpty = -1;
 struct CandWs {
   unsigned int* done;
   unsigned long long* stash_alloc;
+  unsigned long long* ticket;   // stage1 work-item ticket (zeroed by encode)
   int32_t* step_seq;     // [step_cap]
   int64_t* n2;           // [step_cap]
   int32_t* cnt_m;        // [step_cap]
@@ -67,6 +68,7 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   CandWs c;
   c.done = w.take<unsigned int>(1);
   c.stash_alloc = w.take<unsigned long long>(1);
+  c.ticket = w.take<unsigned long long>(1);
   c.step_seq = w.take<int32_t>(step_cap + 1);
   c.n2 = w.take<int64_t>(step_cap + 1);
   c.cnt_m = w.take<int32_t>(step_cap + 1);
@@ -149,8 +151,13 @@ constexpr int kBmWords = 2048;
 static_assert(kBmWords == 2 * kCandCap, "the filter overlays jasc + flo");
 __device__ __forceinline__ uint32_t bm_bit(int32_t tok) { return ((uint32_t)tok * 0x9E3779B1u) >> 16; }
 
+// `own_global`: whether this CTA fills a GLOBAL table. The ranks of a Stage-1 cluster all work on
+// the same step; a global table (a step of > smem_slots/4 content tokens) lives in the step's one
+// workspace region, so only rank 0 clears and fills it and the caller makes the other ranks wait
+// on a cluster barrier before they probe it. Every rank builds its own presence filter.
 __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, int64_t tok_base, int32_t start,
-                             int32_t end, int32_t nbag, int32_t smem_slots = kSmemSlots, uint32_t* bm = nullptr) {
+                             int32_t end, int32_t nbag, int32_t smem_slots = kSmemSlots, uint32_t* bm = nullptr,
+                             bool own_global = true) {
   Table tb;
   uint32_t cap;
   if (nbag <= smem_slots / 4) {
@@ -164,7 +171,9 @@ __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, i
   }
   tb.mask = cap - 1;
   tb.shift = 32u - (31u - __clz(cap));
-  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) tb.slots[i] = make_int2(kEmpty, 0);
+  const bool fill = !tb.global || own_global;
+  if (fill)
+    for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) tb.slots[i] = make_int2(kEmpty, 0);
   if (bm != nullptr)
     for (int i = threadIdx.x; i < kBmWords; i += blockDim.x) bm[i] = 0u;
   __syncthreads();
@@ -175,6 +184,7 @@ __device__ Table build_table(const CandArgs& a, int2* s_tab, const int32_t* t, i
       const uint32_t hb = bm_bit(tok);
       atomicOr(bm + (hb >> 5), 1u << (hb & 31));
     }
+    if (!fill) continue;
     uint32_t slot = hash_slot(tok, tb.shift);
     for (uint32_t probe = 0; probe <= tb.mask; ++probe) {
       int* key = &tb.slots[slot].x;
@@ -218,6 +228,7 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
+    *a.ws.ticket = 0ull;
   }
   for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
     const int32_t s = seq_of_step(a, g);
@@ -299,6 +310,7 @@ __global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {            // stage1's done counter + stash allocator
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
+    *a.ws.ticket = 0ull;
   }
   for (int64_t g = (int64_t)blockIdx.x * kNW + w; g < G; g += (int64_t)gridDim.x * kNW) {
     const int32_t s = seq_of_step(a, g);
@@ -701,7 +713,15 @@ __device__ int4 s1_prefix(const CandArgs& a, int64_t g, int32_t m, int32_t t, in
         v[u] = (q0 + 32 * u < g) ? s1_ld_relaxed(a.ws.lb_agg + q0 + 32 * u) : make_int4(1, 1, 1, 1);
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        while (v[u].x == 0 || v[u].y == 0 || v[u].z == 0) v[u] = s1_ld_relaxed(a.ws.lb_agg + q0 + 32 * u);
+        SpinGuard sg;
+        while (v[u].x == 0 || v[u].y == 0 || v[u].z == 0) {
+          if (sg.expired()) {                          // a predecessor never published: report, do not hang
+            set_status(a.status, MEMSHARE_ERR_CORRUPTION);
+            v[u] = make_int4(1, 1, 1, 1);
+            break;
+          }
+          v[u] = s1_ld_relaxed(a.ws.lb_agg + q0 + 32 * u);
+        }
         rm += v[u].x - 1;
         rt += v[u].y - 1;
         rp += v[u].z - 1;
@@ -744,7 +764,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
-  const int64_t cid = blockIdx.x / csize, ncl = gridDim.x / csize;
   DBG_T(0);
   const int64_t G = total_steps(a);
   __shared__ int4 s_lb;
@@ -770,7 +789,29 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
       if (g != a.seq_step_off[s + 1] - 1) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
     }
   }
-  for (int64_t wi = cid; wi < nwork; wi += ncl) {
+  // Work items come from an atomic ticket (ascending), not a static CTA -> item map: an item's
+  // fused-fill prefix waits only on items with smaller tickets, which running CTAs already hold
+  // and which never wait on larger ones, so progress does not depend on how many CTAs (or
+  // clusters) are co-resident (a static map deadlocks when fewer fit than were launched).
+  __shared__ unsigned long long s_ticket;
+  for (;;) {
+    int64_t wi;
+    if (csize == 1) {
+      __syncthreads();                                     // everyone has read the previous ticket
+      if (threadIdx.x == 0) s_ticket = atomicAdd(a.ws.ticket, 1ull);
+      __syncthreads();
+      wi = (int64_t)s_ticket;
+    } else {
+      cl.sync();                                           // every rank has read rank 0's previous ticket
+      if (crank == 0 && threadIdx.x == 0) s_ticket = atomicAdd(a.ws.ticket, 1ull);
+      cl.sync();
+      wi = (int64_t)*cl.map_shared_rank(&s_ticket, 0);
+    }
+    if (wi >= nwork) {
+      // rank 0 may not exit while another rank still reads its s_ticket over DSMEM
+      if (csize > 1) cl.sync();
+      break;
+    }
     const int64_t g = last_mode ? a.seq_step_off[wi + 1] - 1 : wi;
     if (last_mode && (g < a.seq_step_off[wi] || g >= G)) {            // sequence without steps
       if (fused && crank == 0) publish_nothing(wi);
@@ -789,7 +830,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     const int64_t tok_base = a.seq_tok_off[s];
     const int32_t* t = a.tokens + tok_base;
     const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots,
-                                 sm.u.bm);
+                                 sm.u.bm, crank == 0);
+    if (tb.global && csize > 1) cl.sync();                 // rank 0 filled the shared global table
     DBG_T(1);
     const double n2k = (double)a.ws.n2[g];
     if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
@@ -1180,7 +1222,7 @@ extern "C" memshare_status memshare_step_candidates(
     static int env_cs = -1;
     if (env_cs < 0) { const char* e = getenv("MEMSHARE_S1_CLUSTER"); env_cs = e ? atoi(e) : 0; }
     int cs = 1;
-    if (env_cs > 0 && cur_mode == MEMSHARE_CUR_LAST) cs = env_cs;   // clusters only where tested: LAST rounds
+    if (env_cs > 0 && cur_mode != MEMSHARE_CUR_ALL) cs = env_cs;    // forced (tuning / regression tests)
     else if (cur_mode == MEMSHARE_CUR_LAST)
       for (int c = 8; c > 1; c >>= 1)
         if ((int64_t)num_seqs * c <= sms) { cs = c; break; }
@@ -1210,8 +1252,7 @@ extern "C" memshare_status memshare_step_candidates(
     // (online rounds fuse too: RANGE with the steps as keys -- the non-current ones publish
     // zeros -- and LAST with the sequences as keys, one current step each)
     a.fused = (!half && fused_env() &&
-               ((cur_mode != MEMSHARE_CUR_LAST && cs == 1) ||
-                (cur_mode == MEMSHARE_CUR_LAST && (int64_t)num_seqs <= step_cap + 1))) ? 1 : 0;
+               (cur_mode != MEMSHARE_CUR_LAST || (int64_t)num_seqs <= step_cap + 1)) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
   }

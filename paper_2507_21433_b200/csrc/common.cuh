@@ -29,6 +29,23 @@ __device__ __forceinline__ void set_status(int32_t* st, int32_t code) {
   if (st != nullptr) atomicCAS(st, 0, code);
 }
 
+// Bound on a cross-CTA spin-wait (a flag another CTA publishes). Work is handed out by atomic
+// tickets, so every wait is on a CTA that is already running and the bound is never reached in a
+// correct run; if it is (a bug, a corrupted workspace), the waiter reports CORRUPTION and moves on
+// instead of hanging the device. The clock is read only every 1024 polls.
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  uint32_t n = 0;
+  static constexpr unsigned long long kLimitNs = 2000000000ull;   // 2 s
+  __device__ __forceinline__ bool expired() {
+    if ((++n & 1023u) != 0u) return false;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (t0 == 0) { t0 = t; return false; }
+    return t - t0 > kLimitNs;
+  }
+};
+
 // Bump allocator over the caller's workspace; the same sequence of take() calls in
 // "measure" mode (base == nullptr) gives the required size.
 struct Ws {

@@ -191,6 +191,7 @@ struct AttArgs {
   int32_t stride;
   const int32_t* seq_len;
   int32_t num_seqs, max_chunks;
+  int32_t max_len;    // min(max_seq_len, table_stride * block): the grid and the partials are sized by it
   float scale;
   float* out;
   float* pm;          // [S][h][max_chunks][G]
@@ -244,6 +245,16 @@ __device__ __forceinline__ float bf16_hi(uint32_t x) { return __uint_as_float(x 
 //                 split into bf16 hi + lo parts (two MMAs: ~16-bit P keeps the result within
 //                 fp32-accumulation error of the fp64 oracle); C rows = dims, cols = query heads
 // with an fp32 online softmax in between (row statistics per query head).
+// a seq_len beyond the host max_seq_len (or the table row) would index partials / table entries
+// that were never sized: clamp it and report INVALID_ARGUMENT (one reporter per sequence)
+__device__ __forceinline__ int32_t clamp_len(const AttArgs& a, int32_t len, bool report) {
+  if (len > a.max_len) {
+    if (report) set_status(a.status, MEMSHARE_ERR_INVALID_ARGUMENT);
+    return a.max_len;
+  }
+  return len < 0 ? 0 : len;
+}
+
 template <int DH>
 __global__ void __launch_bounds__(kAttNT) attn_split_kernel(AttArgs a) {
   pdl_trigger();
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kAttNT) attn_split_kernel(AttArgs a) {
   const int chunk = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = a.G;
-  const int32_t len = a.seq_len[s];
+  const int32_t len = clamp_len(a, a.seq_len[s], chunk == 0 && g == 0 && threadIdx.x == 0);
   const int32_t tok0 = chunk * kChunkBlocks * kBlk;
   if (tok0 >= len) return;
   const int r0 = lane >> 2, c2 = 2 * (lane & 3);
@@ -428,7 +439,7 @@ __global__ void attn_combine_kernel(AttArgs a) {
   if (wid >= (int64_t)a.num_seqs * hq) return;
   const int32_t s = (int32_t)(wid / hq), qh = (int32_t)(wid % hq);
   const int g = qh / a.G, qi = qh % a.G;
-  const int32_t len = a.seq_len[s];
+  const int32_t len = clamp_len(a, a.seq_len[s], false);
   float* o = a.out + wid * DH;
   const int nch = len <= 0 ? 0 : (len + kChunkBlocks * kBlk - 1) / (kChunkBlocks * kBlk);
   float M = -INFINITY;
@@ -546,6 +557,10 @@ extern "C" memshare_status memshare_paged_attention_decode(
   a.num_seqs = num_seqs;
   const int chunks = (max_seq_len + kChunkBlocks * kBlk - 1) / (kChunkBlocks * kBlk);
   a.max_chunks = chunks < 1 ? 1 : chunks;
+  {
+    const int64_t row = (int64_t)table_stride * kBlk;
+    a.max_len = row < (int64_t)max_seq_len ? (int32_t)row : max_seq_len;
+  }
   a.scale = scale;
   a.out = out;
   const int64_t parts = (int64_t)num_seqs * num_q_heads * a.max_chunks;

@@ -51,7 +51,7 @@ __device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t cod
 
 struct DistWs {
   unsigned int* ticket;
-  float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]  squared sums (Euclidean) / dot (cosine)
+  float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]  squared sums of t - s (both metrics)
   float* wsn;            // cosine only: [pair_cap][N][2][n_sub][W] source squared norms
   float* wtn;            // cosine only: [target_cap][N][2][n_sub][W] target squared norms
 };
@@ -161,11 +161,21 @@ __device__ __forceinline__ float sum_part(const DistArgs& a, int64_t p, int32_t 
   return sum_warps(a, a.ws.wpart, p, l, kv);
 }
 
-// cosine of one (pair, layer, K|V) from fp32 dot and squared norms, in fp64 (f2 metric, reading R34)
-__device__ __forceinline__ double cos_of(float dot, float tn, float sn) {
-  if (tn == 0.f && sn == 0.f) return 1.0;               // two zero slices are identical
-  if (tn == 0.f || sn == 0.f) return 0.0;
-  return (double)dot / __dsqrt_rn((double)tn * (double)sn);
+// 1 - cos of one (pair, layer, K|V) without cancellation (f2 metric, reading R34): from the
+// squared difference dd = |t-s|^2 (the Euclidean accumulator) and the squared norms tn, sn,
+//   1 - cos = (|t-s|^2 - (|t| - |s|)^2) / (2 |t| |s|)        (law of cosines)
+// whose numerator is a difference of two NON-negative terms with the first >= the second
+// (triangle inequality), so near-duplicate slices keep their relative accuracy, where
+// 1 - dot/(|t||s|) from fp32 sums loses it (at D_cos ~ 4e-4 the latter was ~5e-3 relative).
+// Two zero slices are identical (0); exactly one zero slice is orthogonal (1).
+__device__ __forceinline__ double one_minus_cos(float dd, float tn, float sn) {
+  if (tn == 0.f && sn == 0.f) return 0.0;
+  if (tn == 0.f || sn == 0.f) return 1.0;
+  const double rt = __dsqrt_rn((double)tn), rs = __dsqrt_rn((double)sn);
+  const double diff = rt - rs;
+  double num = (double)dd - diff * diff;
+  if (num < 0.0) num = 0.0;                              // rounding of an exactly-parallel pair
+  return num / (2.0 * rt * rs);
 }
 
 // Finalise target t with the kConsumers threads (tid in [0, kConsumers)); `sync` is the barrier
@@ -186,9 +196,11 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
     if (tid < ppc * N && p < p1) {
       if (a.metric == MEMSHARE_METRIC_COSINE) {
         // f2: PAPER.md:271-273 cosine block similarity, averaged over K|V and layers
-        const double ck = cos_of(sum_part(a, p, l, 0, false), sum_warps(a, a.ws.wtn, t, l, 0), sum_warps(a, a.ws.wsn, p, l, 0));
-        const double cv = cos_of(sum_part(a, p, l, 1, false), sum_warps(a, a.ws.wtn, t, l, 1), sum_warps(a, a.ws.wsn, p, l, 1));
-        terms[tid] = 0.5 * (ck + cv);
+        const double ck = one_minus_cos(sum_part(a, p, l, 0, false), sum_warps(a, a.ws.wtn, t, l, 0),
+                                        sum_warps(a, a.ws.wsn, p, l, 0));
+        const double cv = one_minus_cos(sum_part(a, p, l, 1, false), sum_warps(a, a.ws.wtn, t, l, 1),
+                                        sum_warps(a, a.ws.wsn, p, l, 1));
+        terms[tid] = 0.5 * (ck + cv);                       // mean of (1 - cos_K, 1 - cos_V)
       } else {
         const float sk = sum_part(a, p, l, 0, from_partial);
         const float sv = sum_part(a, p, l, 1, from_partial);
@@ -209,8 +221,8 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
         for (int l2 = lane; l2 < N; l2 += 32) acc += terms[q * N + l2];
         acc = warp_sum(acc);
         if (lane == 0) {
-          // Alg. 1 line 7: return D / N  (cosine metric: D = 1 - mean similarity)
-          const float D = (float)(a.metric == MEMSHARE_METRIC_COSINE ? 1.0 - acc / (double)N : acc / (double)N);
+          // Alg. 1 line 7: return D / N  (cosine metric: the layer mean of 1 - cos)
+          const float D = (float)(acc / (double)N);
           a.distance[pp] = D;
           a.under[pp] = D < a.tau_b ? 1 : 0;
         }
@@ -373,7 +385,7 @@ template <int KRE, int MET>
 __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (&x)[KRE], float2 (&T)[KRE * 4],
                                         int warp, int lane) {
   if (MET == MEMSHARE_METRIC_COSINE) {
-    // f2 (reading R34): target stage -> cache + squared norm; source stage -> dot + squared norm
+    // f2 (reading R34): target stage -> cache + squared norm; source stage -> |t - s|^2 + squared norm
     const int64_t o = (int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp;
     float2 n0 = make_float2(0.f, 0.f), n1 = n0;
     if (h.w & H_ANCHOR) {
@@ -387,18 +399,21 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
       const float tn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
       if (lane == 0) a.ws.wtn[o] = tn;
     } else if (h.w & H_PAIR) {
-      float2 d0 = make_float2(0.f, 0.f), d1 = d0;
+      // squared difference (the same accumulator as the Euclidean metric) and the source norm
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
       for (int r = 0; r < KRE; ++r) {
         const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
-        d0 = __ffma2_rn(T[4 * r + 0], f0, d0); d1 = __ffma2_rn(T[4 * r + 1], f1, d1);
-        d0 = __ffma2_rn(T[4 * r + 2], f2, d0); d1 = __ffma2_rn(T[4 * r + 3], f3, d1);
+        const float2 e0 = sub_bf2(x[r].x, T[4 * r + 0]), e1 = sub_bf2(x[r].y, T[4 * r + 1]);
+        const float2 e2 = sub_bf2(x[r].z, T[4 * r + 2]), e3 = sub_bf2(x[r].w, T[4 * r + 3]);
+        acc0 = __ffma2_rn(e0, e0, acc0); acc1 = __ffma2_rn(e1, e1, acc1);
+        acc0 = __ffma2_rn(e2, e2, acc0); acc1 = __ffma2_rn(e3, e3, acc1);
         n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
         n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
       }
-      const float dot = warp_sum((d0.x + d0.y) + (d1.x + d1.y));
+      const float dd = warp_sum((acc0.x + acc0.y) + (acc1.x + acc1.y));
       const float sn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
-      if (lane == 0) { a.ws.wpart[o] = dot; a.ws.wsn[o] = sn; }
+      if (lane == 0) { a.ws.wpart[o] = dd; a.ws.wsn[o] = sn; }
     }
     return;
   }

@@ -60,7 +60,7 @@ __device__ __forceinline__ Agg shfl_agg_down(const Agg& v, int o) {
 }
 
 struct SegWs {
-  int32_t* flag;   // [tiles] 0 = nothing, 1 = aggregate, 2 = inclusive prefix (zeroed per call)
+  int32_t* flag;   // [tiles] 0 = nothing, 1 = aggregate, 2 = inclusive prefix; [tiles] = tile ticket (zeroed per call)
   int4* agg;       // [tiles]
   int4* inc;       // [tiles]
 };
@@ -170,11 +170,17 @@ __global__ void __launch_bounds__(kNT, 1) seg_kernel(SegArgs a) {
   __shared__ Agg s_tile_prefix;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t tiles = (a.num_tokens + kTile - 1) / kTile;
-  const int64_t tile = blockIdx.x;
   if (tiles == 0) {                                      // no tokens: every sequence has 0 steps
     for (int32_t s = threadIdx.x; s <= a.num_seqs; s += kNT) a.seq_step_off[s] = 0;
     return;
   }
+  // the tile comes from an atomic ticket (flag[tiles], zeroed with the flags), not blockIdx: a
+  // tile's look-back waits only on tiles already claimed by running CTAs, so the scan completes
+  // however many CTAs are co-resident
+  __shared__ int32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ws.flag + tiles, 1);
+  __syncthreads();
+  const int64_t tile = s_tile;
   const int64_t i0 = tile * kTile + (int64_t)threadIdx.x * kItems;
   const bool live = i0 < a.num_tokens;
   SeqCur q{};
@@ -240,7 +246,13 @@ __global__ void __launch_bounds__(kNT, 1) seg_kernel(SegArgs a) {
         const int64_t qi = p - lane;
         int32_t f = 2;
         if (qi >= 0) {
+          SpinGuard sg;
           while ((f = ld_acquire(a.ws.flag + qi)) == 0) {
+            if (sg.expired()) {                          // never published: report, do not hang
+              set_status(a.status, MEMSHARE_ERR_CORRUPTION);
+              f = 2;
+              break;
+            }
           }
         }
         const unsigned inc_mask = __ballot_sync(0xffffffffu, f == 2);
@@ -362,7 +374,7 @@ extern "C" memshare_status memshare_segment_steps(const int32_t* tokens, int64_t
   const int64_t tiles = (num_tokens + kTile - 1) / kTile;
   // the look-back flags are zeroed by a small kernel, not a memset node: it keeps the launch chain
   // programmatic (seg_kernel's CTAs wait for it to complete before they publish)
-  if (tiles > 0) launch_pdl(flag_reset_kernel, dim3(1), dim3(256), 0, st, a.ws.flag, tiles);
+  if (tiles > 0) launch_pdl(flag_reset_kernel, dim3(1), dim3(256), 0, st, a.ws.flag, tiles + 1);   // + the ticket
   launch_pdl(seg_kernel, dim3((unsigned)(tiles < 1 ? 1 : tiles)), dim3(kNT), 0, st, a);
   return launch_status();
 }

@@ -151,6 +151,20 @@ def make_batch(seed: int, num_seqs: int, lengths, gen_start: int, block_size: in
                       step_starts=starts, copy_of=copies)
 
 
+def concat(batches) -> TraceBatch:
+    """The sequences of several batches (same vocabulary and delimiters) as one batch, in order."""
+    toks = [b.tokens for b in batches]
+    off = np.zeros(sum(b.num_seqs for b in batches) + 1, np.int64)
+    lens = [int(b.seq_tok_off[i + 1] - b.seq_tok_off[i]) for b in batches for i in range(b.num_seqs)]
+    off[1:] = np.cumsum(lens)
+    return TraceBatch(tokens=np.concatenate(toks).astype(np.int32) if toks else np.zeros(0, np.int32),
+                      seq_tok_off=off, gen_start=np.concatenate([b.gen_start for b in batches]).astype(np.int32),
+                      final=np.concatenate([b.final for b in batches]).astype(np.uint8),
+                      delim_ids=batches[0].delim_ids, vocab=batches[0].vocab,
+                      step_starts=[x for b in batches for x in b.step_starts],
+                      copy_of=[x for b in batches for x in b.copy_of])
+
+
 def tiny_t0() -> TraceBatch:
     """The hand-built T0 fixture (SURVEY.md §8(d) "tiny (T0)"; BASELINE.json configs[0]).
 

@@ -122,6 +122,37 @@ def c4(num_seqs: int = 128, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8
     return _paged(f"c4_phi4_{num_seqs}xaime", kv.PHI4, b, seed, eta, tau_s)
 
 
+# ---------------------------------------------------------------------------- partitionable batches
+# configs[2..4] are batches of independent sequences that the bench splits over GPUs and waves.
+# Sequence i of a batch is generated from its own seed, so any subset (a rank's share, a wave) is
+# the same sequences wherever it runs.
+BATCHES = {
+    # name: (BASELINE configs index, sequences, shape, vocab, length of sequence i, seed of sequence i)
+    "c3": (2, 64, kv.QWEN32B, traces.QWEN_VOCAB, lambda seed, i: 12288, lambda seed, i: seed * 1000 + i),
+    "c4": (3, 128, kv.PHI4, traces.PHI4_VOCAB,
+           lambda seed, i: int(np.random.default_rng(seed + 4).integers(8192, 16621, 128)[i]),
+           lambda seed, i: seed * 1000 + 200 + i),
+    "c5": (4, 512, kv.QWEN32B, traces.QWEN_VOCAB, lambda seed, i: 16384, lambda seed, i: seed * 1000 + 500 + i),
+}
+
+
+def batch_traces(config: str, indices, seed: int = 0) -> traces.TraceBatch:
+    """Token traces of sequences `indices` of batch `config` (128-token prompt each)."""
+    _, _, shape, vocab, length, sseed = BATCHES[config]
+    return traces.concat([traces.make_batch(sseed(seed, int(i)), 1, length(seed, int(i)), 128, shape.block_size,
+                                            vocab=vocab) for i in indices])
+
+
+def batch(config: str, indices, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8) -> Workload:
+    """Workload (trace, paged table, KV generator state) of sequences `indices` of batch `config`."""
+    _, n, shape, _, _, _ = BATCHES[config]
+    idx = [int(i) for i in indices]
+    assert all(0 <= i < n for i in idx), idx
+    w = _paged(f"{config}_{len(idx)}of{n}", shape, batch_traces(config, idx, seed), seed, eta, tau_s)
+    w.indices = idx
+    return w
+
+
 def small(shape: kv.KVShape, num_seqs: int, length: int, seed: int = 0, eta: float = 0.05, tau_s: float = 0.8,
           gen_start: int = 64, **kw) -> Workload:
     """Parity-size workloads: several tiles and ragged tails, oracle-checkable in seconds."""

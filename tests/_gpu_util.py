@@ -66,23 +66,62 @@ def compare_distances(gpu_D, ora_D):
     return float(rel.max()) if rel.size else 0.0
 
 
-def compare_decisions(gpu_dec, ora_D, target_off, src_logical, tau_b):
-    """Decisions equal except near-threshold / near-tie targets, which are counted and returned."""
+def compare_decisions(gpu_dec, gpu_D, ora_D, target_off, pairs, tau_b):
+    """Per-target decisions (PAPER.md:319-320 "selecting those with minimal distances", reading R22;
+    accept iff D < tau_b, R21) against the oracle on the same pairs.
+
+    `pairs` holds the oracle's pair records (seq, target_logical, target_phys, source_logical,
+    source_phys) aligned with `ora_D` / `gpu_D`, grouped by `target_off`. Checked per target:
+      * the target identity (seq, target_logical, target_phys) and num_candidates: exact;
+      * the GPU's pick is one of the target's pairs (source_logical AND source_phys), its recorded
+        distance is bit-equal to the GPU's per-pair distance and within DIST_RTOL of the oracle's;
+      * the pick is the argmin of the GPU's own distances with exact ties -> smaller source
+        logical (the rule, enforced exactly on the GPU's values);
+      * the pick lies in the oracle's tie set: D_oracle[pick] <= D_min (1 + NEAR_TIE); where the
+        oracle minimum is exactly 0 (bit-identical blocks: both sides compute 0 exactly) the pick
+        must BE the oracle's (the smallest source logical among the zeros);
+      * accepted == (GPU distance < fp32 tau_b) exactly, and equals the oracle's decision unless
+        the oracle's best distance is within NEAR_THRESH of tau_b.
+    Returns (near_threshold, near_tie) counts (reported, not failed)."""
+    src_logical = np.asarray(pairs["source_logical"])
+    gpu_D = np.asarray(gpu_D, np.float32)
     best, acc, _ = oracle.select(ora_D, target_off, src_logical, tau_b)
     near_thresh = near_tie = 0
-    tb = float(np.float32(tau_b))
+    tb32 = np.float32(tau_b)
+    tb = float(tb32)
     for t in range(target_off.size - 1):
-        p0, p1 = target_off[t], target_off[t + 1]
-        Ds = np.sort(ora_D[p0:p1])
-        tie = Ds.size > 1 and (Ds[1] - Ds[0]) <= NEAR_TIE * max(Ds[1], 1e-30)
-        thr = abs(ora_D[best[t]] - tb) <= NEAR_THRESH * tb
-        src_ok = gpu_dec["source_logical"][t] == src_logical[best[t]]
-        acc_ok = bool(gpu_dec["accepted"][t]) == bool(acc[t])
-        if not src_ok:
-            assert tie, f"target {t}: source differs without a near tie"
+        p0, p1 = int(target_off[t]), int(target_off[t + 1])
+        ob = int(best[t])
+        for k in ("seq", "target_logical", "target_phys"):
+            assert gpu_dec[k][t] == pairs[k][ob], f"target {t}: {k} {gpu_dec[k][t]} != {pairs[k][ob]}"
+        assert gpu_dec["num_candidates"][t] == p1 - p0, f"target {t}: num_candidates"
+        hit = np.nonzero(src_logical[p0:p1] == gpu_dec["source_logical"][t])[0]
+        assert hit.size == 1, f"target {t}: GPU source logical {gpu_dec['source_logical'][t]} is not a candidate"
+        g = p0 + int(hit[0])
+        assert gpu_dec["source_phys"][t] == pairs["source_phys"][g], f"target {t}: source_phys"
+        gdist = np.float32(gpu_dec["distance"][t])
+        assert gdist.view(np.uint32) == gpu_D[g].view(np.uint32), f"target {t}: decision distance != pair distance"
+        if ora_D[g] == 0.0:
+            assert gdist == 0.0, f"target {t}: identical blocks must give 0"
+        else:
+            assert abs(float(gdist) - ora_D[g]) <= DIST_RTOL * ora_D[g], f"target {t}: decision distance"
+        # the GPU's own argmin with the smaller-logical tie rule, exactly
+        seg = gpu_D[p0:p1]
+        m = seg.min()
+        cand = np.nonzero(seg == m)[0]
+        exp_g = p0 + int(cand[np.argmin(src_logical[p0:p1][cand])])
+        assert g == exp_g, f"target {t}: GPU pick {g} is not its own argmin / smallest-logical tie {exp_g}"
+        # the oracle's tie set
+        dmin = float(ora_D[p0:p1].min())
+        if dmin == 0.0:
+            assert g == ob, f"target {t}: exact D == 0 tie must go to the smaller source logical"
+        else:
+            assert ora_D[g] <= dmin * (1.0 + NEAR_TIE), f"target {t}: GPU pick D={ora_D[g]!r} outside the tie set of {dmin!r}"
+        if g != ob:
             near_tie += 1
-        if not acc_ok:
-            assert thr, f"target {t}: accept differs away from the threshold"
+        assert bool(gpu_dec["accepted"][t]) == bool(gdist < tb32), f"target {t}: accepted != (D < tau_b)"
+        if bool(gpu_dec["accepted"][t]) != bool(acc[t]):
+            assert abs(ora_D[ob] - tb) <= NEAR_THRESH * tb, f"target {t}: accept differs away from the threshold"
             near_thresh += 1
     return near_thresh, near_tie
 

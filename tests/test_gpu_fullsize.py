@@ -62,7 +62,7 @@ def sampled_parity(w, n_targets=24, seed=0):
     compare_distances(gd["distance"][psel], D)
     sub_off = np.concatenate([[0], np.cumsum([toff[t + 1] - toff[t] for t in tsel])])
     sub_dec = {k: v[tsel] for k, v in gd["decisions"].items()}
-    near = compare_decisions(sub_dec, D, sub_off, pr["source_logical"][psel], w.tau_b)
+    near = compare_decisions(sub_dec, gd["distance"][psel], D, sub_off, {k: v[psel] for k, v in pr.items()}, w.tau_b)
     s = p.read_state()
     st_o, tab, rc, fl, fc, nf, af = oracle.remap(w.table, w.refcount, w.free_list, w.free_count, gd["decisions"],
                                                  sh.block_size)
