@@ -218,7 +218,7 @@ __device__ __forceinline__ int64_t fill_keys(const CandArgs& a, int64_t G) {
 // One CTA per step (latency-optimal when the steps fit in one wave: a single CoT).
 __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(2);
   extern __shared__ int2 s_tab[];                         // [kSmemSlots]
   __shared__ int64_t sh[kNW + 1];
   const int64_t G = total_steps(a);
@@ -300,7 +300,7 @@ __device__ int64_t warp_step_n2(const CandArgs& a, int2* s_tab, const int32_t* t
 
 __global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(2);
   extern __shared__ int2 s_tab[];                         // [kSmemSlots] = kNW warps x kEncSlots
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t G = total_steps(a);
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   static_assert(NT != 1024 || kMaxTgt * 16 <= S1Cfg<1024>::kTok * 4, "fused fill reuses the staging area");
   const bool fused = NT == 1024 && a.fused != 0;   // the 512-thread shape never fuses
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(3);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelSmem<NT>& sm = *reinterpret_cast<SelSmem<NT>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1045,7 +1045,7 @@ struct FillSmem {
 
 __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(4);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FillSmem& sm = *reinterpret_cast<FillSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1112,6 +1112,8 @@ __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
 }  // namespace ms
 
 using namespace ms;
+
+TL_EXPORT(candidates)
 
 extern "C" int memshare_debug_stage1_tok(long long* host, int n) {
   if (n > 2048 * 32) n = 2048 * 32;

@@ -147,6 +147,48 @@ __device__ void cta_scan_counts(const int32_t* cnt, int64_t* out_off, int64_t n,
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Tuning only (-DMS_TIMELINE variant library): per-kernel device timestamps of one round --
+// [id][0] first CTA resident, [id][1] first CTA past its dependency wait, [id][2] last CTA done
+// (globaltimer ns); read with memshare_debug_tl_<file>(). No effect in the shipped library.
+#ifdef MS_TIMELINE
+static __device__ unsigned long long ms_tl[16][4];
+__device__ __forceinline__ unsigned long long ms_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_WAIT(id)                                                       \
+  do {                                                                    \
+    if (threadIdx.x == 0) atomicMin(&::ms::ms_tl[id][0], ::ms::ms_gtime()); \
+    ::ms::pdl_wait();                                                     \
+    if (threadIdx.x == 0) atomicMin(&::ms::ms_tl[id][1], ::ms::ms_gtime()); \
+  } while (0)
+#define TL_END(id)                                                        \
+  do {                                                                    \
+    if (threadIdx.x == 0) atomicMax(&::ms::ms_tl[id][2], ::ms::ms_gtime()); \
+  } while (0)
+struct TlGuard {
+  int id;
+  __device__ ~TlGuard() { TL_END(id); }
+};
+#define TL_SCOPE(id) TL_WAIT(id); ::ms::TlGuard _ms_tl_guard{id}
+#define TL_EXPORT(name)                                                                         \
+  extern "C" int memshare_debug_tl_##name(unsigned long long* host, int reset) {               \
+    int e = (int)cudaMemcpyFromSymbol(host, ::ms::ms_tl, sizeof(::ms::ms_tl));                 \
+    if (reset) {                                                                                \
+      unsigned long long init[16][4];                                                           \
+      for (int i = 0; i < 16; ++i) { init[i][0] = init[i][1] = ~0ull; init[i][2] = init[i][3] = 0ull; } \
+      e |= (int)cudaMemcpyToSymbol(::ms::ms_tl, init, sizeof(init));                            \
+    }                                                                                           \
+    return e;                                                                                   \
+  }
+#else
+#define TL_WAIT(id) ::ms::pdl_wait()
+#define TL_END(id) do { } while (0)
+#define TL_SCOPE(id) ::ms::pdl_wait()
+#define TL_EXPORT(name)
+#endif
+
 inline bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {

@@ -443,6 +443,21 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
   }
 }
 
+#ifdef MS_DIST_NOEVAL
+// tuning only (-DMS_DIST_NOEVAL variant): consume the loaded stage without the arithmetic (the
+// words are folded so the loads stay), to separate the pipeline + shared-memory cost from the math
+template <int KRE, int MET>
+__device__ __forceinline__ void st_eval_probe(const DistArgs& a, int4 h, const uint4 (&x)[KRE], int warp, int lane) {
+  uint32_t f = 0u;
+#pragma unroll
+  for (int r = 0; r < KRE; ++r) f ^= x[r].x ^ x[r].y ^ x[r].z ^ x[r].w;
+  if (f == 0x9E3779B9u && (h.w & H_PAIR)) a.ws.wpart[(int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp] = 1.f;
+}
+#define ST_EVAL(h, x) st_eval_probe<KRE, MET>(a, h, x, warp, lane)
+#else
+#define ST_EVAL(h, x) st_eval<KRE, MET>(a, h, x, T, warp, lane)
+#endif
+
 template <int KRE, int MET, bool PARTIAL>
 __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
   constexpr int NS = StCfg<KRE>::kNSt;
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
   }
   __syncthreads();
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(6);
   if (warp == kConsumerWarps) {
     st_producer<KRE>(sm, a, lane);
     return;
@@ -499,13 +514,13 @@ __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
     mbar_wait(&sm.full[stage], ph);
     hb = sm.hdr[stage];
     if (!(hb.w & H_STOP)) load(xb, hb.z);
-    st_eval<KRE, MET>(a, ha, xa, T, warp, lane);
+    ST_EVAL(ha, xa);
     if (hb.w & H_STOP) break;
     release();
     mbar_wait(&sm.full[stage], ph);
     ha = sm.hdr[stage];
     if (!(ha.w & H_STOP)) load(xa, ha.z);
-    st_eval<KRE, MET>(a, hb, xb, T, warp, lane);
+    ST_EVAL(hb, xb);
     if (ha.w & H_STOP) break;
     release();
   }
@@ -519,13 +534,13 @@ __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
 // before they take tickets).
 __global__ void ticket_reset_kernel(unsigned int* ticket) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(5);
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
 __global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int from_partial) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(7);
   __shared__ double terms[kConsumers];
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
   for (int64_t t = blockIdx.x; t < T; t += gridDim.x)
@@ -599,6 +614,8 @@ static cudaError_t launch_st_any(int kre, bool partial, int metric, const DistAr
 }  // namespace ms
 
 using namespace ms;
+
+TL_EXPORT(distance)
 
 static thread_local cudaEvent_t g_prof_begin = nullptr, g_prof_end = nullptr;
 

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kNT) remap_kernel(int32_t* __restrict__ table,
                                                     int32_t block_size, int64_t* __restrict__ num_freed,
                                                     int64_t* __restrict__ affected, RemapWs ws, int32_t* status) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(8);
   __shared__ int64_t sh[kNT / 32 + 1];
   __shared__ int bad;
   int64_t T = *num_targets;
@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(kNT) remap_kernel(int32_t* __restrict__ table,
 }  // namespace ms
 
 using namespace ms;
+
+TL_EXPORT(remap)
 
 extern "C" size_t memshare_remap_workspace_size(int32_t num_blocks, int64_t target_cap) {
   if (num_blocks < 0 || target_cap < 0) return 0;

@@ -165,7 +165,7 @@ __device__ __forceinline__ Agg ld_agg(const int4* p) {
 
 __global__ void __launch_bounds__(kNT, 1) seg_kernel(SegArgs a) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(1);
   __shared__ Agg s_warp[kNT / 32];
   __shared__ Agg s_tile_prefix;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kNT, 1) seg_kernel(SegArgs a) {
 // zeroes the look-back flags (a kernel, not a memset node: keeps the launch chain programmatic)
 __global__ void flag_reset_kernel(int32_t* flag, int64_t n) {
   pdl_trigger();
-  pdl_wait();
+  TL_SCOPE(0);
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) flag[i] = 0;
 }
 
@@ -337,6 +337,8 @@ __global__ void flag_reset_kernel(int32_t* flag, int64_t n) {
 }  // namespace ms
 
 using namespace ms;
+
+TL_EXPORT(segment)
 
 
 extern "C" size_t memshare_segment_steps_workspace_size(int64_t num_tokens, int32_t num_seqs, int64_t step_cap) {

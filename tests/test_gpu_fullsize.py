@@ -1,7 +1,7 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py uses.
 
-c3 (QwQ-32B shape, 12,288-token CoTs) as one single-GPU wave of 32 sequences (96 GiB pool) and
-c4 (Phi-4-reasoning-plus shape, AIME-length traces) with 32 sequences: segmentation, Stage-1
+c3 (QwQ-32B shape, the 64-sequence batch as bench.py's two N = 1 waves), c4 (Phi-4-reasoning-
+plus shape, all 128 AIME-length traces in bench.py's waves) and a c5 wave: segmentation, Stage-1
 matches and block pairs are compared in full (bit-exact); distances and decisions on a seeded
 sample of whole targets the oracle computes one by one (only their blocks are copied to the
 host); the remap in full on the GPU's own decisions.
@@ -75,14 +75,31 @@ def sampled_parity(w, n_targets=24, seed=0):
     torch.cuda.empty_cache()
 
 
-def test_c3_one_wave_32_sequences():
-    sampled_parity(workloads.c3(num_seqs=32, seed=0))
+def _plan(cfg, n):
+    import torch
+
+    import bench
+    bins, W, _ = bench.plan_waves(cfg, n, 1, 0, torch.device("cuda", 0))
+    return bins
 
 
-def test_c4_phi4_32_sequences():
-    sampled_parity(workloads.c4(num_seqs=32, seed=0))
+def test_c3_bench_waves_64_targets():
+    """configs[2]: the 64-sequence QwQ-32B batch, both waves of bench.py's N = 1 plan (LPT on
+    Stage-1 pair counts, ~32 sequences / 103 GB of KV each), 64 sampled targets per wave."""
+    for wi, idx in enumerate(_plan("c3", 64)):
+        sampled_parity(workloads.batch("c3", idx, 0), n_targets=64, seed=wi)
+
+
+def test_c4_phi4_all_128_traces():
+    """configs[3]: all 128 Phi-4-reasoning-plus AIME-length traces (~430 GB of KV) as bench.py's
+    waves, 48 sampled targets per wave."""
+    bins = _plan("c4", 128)
+    assert sorted(i for b in bins for i in b) == list(range(128))
+    for wi, idx in enumerate(bins):
+        sampled_parity(workloads.batch("c4", idx, 0), n_targets=48, seed=wi)
 
 
 def test_c5_one_wave_32_sequences():
-    """configs[4]: 32 x 16,384-token CoTs at the 32B shape (one per-GPU wave, 137 GB pool)."""
-    sampled_parity(workloads.c5(num_seqs=32, seed=0))
+    """configs[4]: 32 x 16,384-token CoTs at the 32B shape (one per-GPU wave, 137 GB pool), 64
+    sampled targets."""
+    sampled_parity(workloads.batch("c5", list(range(32)), 0), n_targets=64)
