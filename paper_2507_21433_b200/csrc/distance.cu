@@ -30,11 +30,15 @@
 namespace ms {
 namespace {
 
-constexpr int kConsumerWarps = 8;
-static_assert(kConsumerWarps % 4 == 0, "partials are read as float4");
+constexpr int kConsumerWarps = 8;                            // consumer warps of the default instantiations
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kThreads = kConsumers + 32;                  // + the producer warp
 constexpr int kChunkUnit = 16 * kConsumers;                 // 4 KiB: one 16-byte chunk per consumer thread
+constexpr int kFinThreads = 256;                            // finalisation CTA
+constexpr int kFinWarps = kFinThreads / 32;
+// A 40 KiB slice (Phi-4-reasoning-plus: 16 x 10 x 128 x 2 B) is one stage for TEN consumer warps of
+// 8 chunks each -- the same registers per thread as the 32 KiB slices with eight warps (eight warps
+// would need 10 chunks each: 84 bytes of spills at the 168-register cap of 288 threads).
+constexpr int kPhi4Slice = 40960;
 constexpr int kRingBytes = 224 * 1024;                      // shared-memory ring (of 227 KB per CTA)
 constexpr int kMaxKre = 10;                                 // largest stage: 40 KiB (one Phi-4 slice)
 constexpr int kMaxRingStages = 48;
@@ -51,15 +55,16 @@ __device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t cod
 
 struct DistWs {
   unsigned int* ticket;
-  float* wpart;          // [pair_cap][N][2][n_sub][kConsumerWarps]  squared sums of t - s (both metrics)
+  float* wpart;          // [pair_cap][N][2][n_sub][wstride]  per consumer warp: squared sums of t - s (both metrics)
   float* wsn;            // cosine only: [pair_cap][N][2][n_sub][W] source squared norms
   float* wtn;            // cosine only: [target_cap][N][2][n_sub][W] target squared norms
 };
 
-DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int64_t pair_cap, int64_t target_cap, int32_t metric) {
+DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t wstride, int64_t pair_cap, int64_t target_cap,
+                   int32_t metric) {
   DistWs d;
   d.ticket = w.take<unsigned int>(1);
-  const size_t per = (size_t)N * 2 * n_sub * kConsumerWarps;
+  const size_t per = (size_t)N * 2 * n_sub * wstride;
   d.wpart = w.take<float>((size_t)pair_cap * per + 1);
   const bool cosine = metric == MEMSHARE_METRIC_COSINE;
   d.wsn = w.take<float>(cosine ? (size_t)pair_cap * per + 1 : 1);
@@ -75,6 +80,7 @@ struct DistArgs {
   int32_t num_blocks;
   int32_t N, d, h_global;
   int32_t slice_bytes, n_sub;
+  int32_t cw, wstride;   // consumer warps of the streaming kernel; partials per (pair, layer, K|V, sub) (4 | wstride)
   int32_t lpi, n_chunks;
   const memshare_block_pair* pairs;
   const int64_t* target_off;
@@ -136,14 +142,18 @@ __device__ __forceinline__ int64_t clamp_count(const int64_t* p, int64_t cap) {
 
 // fixed-order fp32 sum of the per-warp partials of (row, layer l, kv) of one workspace buffer
 __device__ __forceinline__ float sum_warps(const DistArgs& a, const float* buf, int64_t row, int32_t l, int32_t kv) {
-  const float4* w = reinterpret_cast<const float4*>(buf + (((row * a.N + l) * 2 + kv) * a.n_sub) * kConsumerWarps);
+  const int q4 = a.wstride / 4;
+  const float4* w = reinterpret_cast<const float4*>(buf + (((row * a.N + l) * 2 + kv) * a.n_sub) * a.wstride);
   float s = 0.f;
   for (int sub = 0; sub < a.n_sub; ++sub) {
-    float4 v[kConsumerWarps / 4];
-#pragma unroll
-    for (int j = 0; j < kConsumerWarps / 4; ++j) v[j] = __ldcg(w + sub * (kConsumerWarps / 4) + j);
-#pragma unroll
-    for (int j = 0; j < kConsumerWarps / 4; ++j) s = (((s + v[j].x) + v[j].y) + v[j].z) + v[j].w;
+    for (int j = 0; j < q4; ++j) {                       // warps 0 .. cw-1 in order (the padding is skipped)
+      const float4 v = __ldcg(w + sub * q4 + j);
+      const int c = a.cw - 4 * j;
+      s = s + v.x;
+      if (c > 1) s = s + v.y;
+      if (c > 2) s = s + v.z;
+      if (c > 3) s = s + v.w;
+    }
   }
   return s;
 }
@@ -178,7 +188,7 @@ __device__ __forceinline__ double one_minus_cos(float dd, float tn, float sn) {
   return num / (2.0 * rt * rs);
 }
 
-// Finalise target t with the kConsumers threads (tid in [0, kConsumers)); `sync` is the barrier
+// Finalise target t with the kFinThreads threads (tid in [0, kFinThreads)); `sync` is the barrier
 // among exactly those threads.
 template <class Sync>
 __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int tid, bool from_partial, Sync sync) {
@@ -187,7 +197,7 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
   int64_t p1 = __ldcg(a.target_off + t + 1);
   if (p1 > P) p1 = P;
   const int N = a.N;
-  const int ppc = kConsumers / N;                       // whole pairs per chunk
+  const int ppc = kFinThreads / N;                      // whole pairs per chunk
   const double inv = 1.0 / (2.0 * (double)a.d * (double)a.h_global);
   const int lane = tid & 31, w = tid >> 5;
   for (int64_t pc = p0; pc < p1; pc += ppc) {
@@ -214,7 +224,7 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
     }
     sync();
     if (a.mode != MEMSHARE_DIST_PARTIAL) {
-      for (int q = w; q < ppc; q += kConsumerWarps) {
+      for (int q = w; q < ppc; q += kFinWarps) {
         const int64_t pp = pc + q;
         if (pp >= p1) break;
         double acc = 0.0;
@@ -278,23 +288,23 @@ __device__ __forceinline__ float2 sub_bf2(uint32_t x, float2 t) {
   return d;
 }
 
-template <int KRE>
+template <int KRE, int CW = kConsumerWarps>
 struct StCfg {
-  static constexpr int kStageB = KRE * kChunkUnit;
+  static constexpr int kStageB = KRE * 16 * 32 * CW;
   static constexpr int kNSt = (kRingBytes / kStageB) < kMaxRingStages ? kRingBytes / kStageB : kMaxRingStages;
 };
 
-template <int KRE>
+template <int KRE, int CW>
 struct StSmem {
-  alignas(128) uint8_t ring[StCfg<KRE>::kNSt][StCfg<KRE>::kStageB];
-  alignas(16) int4 hdr[StCfg<KRE>::kNSt];
-  alignas(8) uint64_t full[StCfg<KRE>::kNSt];
-  uint64_t empty[StCfg<KRE>::kNSt];
+  alignas(128) uint8_t ring[StCfg<KRE, CW>::kNSt][StCfg<KRE, CW>::kStageB];
+  alignas(16) int4 hdr[StCfg<KRE, CW>::kNSt];
+  alignas(8) uint64_t full[StCfg<KRE, CW>::kNSt];
+  uint64_t empty[StCfg<KRE, CW>::kNSt];
 };
 
-template <int KRE>
-__device__ __forceinline__ void st_producer(StSmem<KRE>& sm, const DistArgs& a, int lane) {
-  constexpr int NS = StCfg<KRE>::kNSt;
+template <int KRE, int CW>
+__device__ __forceinline__ void st_producer(StSmem<KRE, CW>& sm, const DistArgs& a, int lane) {
+  constexpr int NS = StCfg<KRE, CW>::kNSt;
   const int64_t I = clamp_count(a.num_targets, a.target_cap);
   const int64_t Pn = clamp_count(a.num_pairs, a.pair_cap);
   const int64_t total = I * a.n_chunks;
@@ -344,9 +354,9 @@ __device__ __forceinline__ void st_producer(StSmem<KRE>& sm, const DistArgs& a, 
           for (int32_t kv = 0; kv < 2; ++kv) {
             const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
             for (int32_t sub = 0; sub < a.n_sub; ++sub) {
-              const int32_t boff = sub * StCfg<KRE>::kStageB;
-              const int32_t bytes = (a.slice_bytes - boff) < StCfg<KRE>::kStageB ? a.slice_bytes - boff
-                                                                                   : StCfg<KRE>::kStageB;
+              const int32_t boff = sub * StCfg<KRE, CW>::kStageB;
+              const int32_t bytes = (a.slice_bytes - boff) < StCfg<KRE, CW>::kStageB ? a.slice_bytes - boff
+                                                                                       : StCfg<KRE, CW>::kStageB;
               for (int32_t q = -1; q < cn; ++q) {                 // q = -1: the target
                 const int32_t v = __shfl_sync(0xffffffffu, (q & 32) ? sb : sa, q < 0 ? 0 : (q & 31));
                 if (lane == 0) {
@@ -355,7 +365,7 @@ __device__ __forceinline__ void st_producer(StSmem<KRE>& sm, const DistArgs& a, 
                   // target (cosine: its squared norm)
                   const int64_t po = q < 0 ? cur.t : (int64_t)(cur.lo + c0 + q);
                   mbar_wait(&sm.empty[stage], ph ^ 1u);
-                  sm.hdr[stage] = make_hdr((((po * a.N + l) * 2 + kv) * a.n_sub + sub) * kConsumerWarps, bytes,
+                  sm.hdr[stage] = make_hdr((((po * a.N + l) * 2 + kv) * a.n_sub + sub) * a.wstride, bytes,
                                            q < 0 ? H_ANCHOR : H_PAIR);
                   mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
                   bulk_g2s(sm.ring[stage], base + (int64_t)phys * a.block_stride_b + boff, (uint32_t)bytes,
@@ -458,25 +468,26 @@ __device__ __forceinline__ void st_eval_probe(const DistArgs& a, int4 h, const u
 #define ST_EVAL(h, x) st_eval<KRE, MET>(a, h, x, T, warp, lane)
 #endif
 
-template <int KRE, int MET, bool PARTIAL>
-__global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
-  constexpr int NS = StCfg<KRE>::kNSt;
+template <int KRE, int CW, int MET, bool PARTIAL>
+__global__ void __launch_bounds__(CW * 32 + 32, 1) distance_st_kernel(DistArgs a) {
+  constexpr int NS = StCfg<KRE, CW>::kNSt;
+  constexpr int NC = CW * 32;                            // consumer threads
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  StSmem<KRE>& sm = *reinterpret_cast<StSmem<KRE>*>(smem_raw);
+  StSmem<KRE, CW>& sm = *reinterpret_cast<StSmem<KRE, CW>*>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kConsumerWarps);
+      mbar_init(&sm.empty[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   pdl_trigger();
   TL_SCOPE(6);
-  if (warp == kConsumerWarps) {
-    st_producer<KRE>(sm, a, lane);
+  if (warp == CW) {
+    st_producer<KRE, CW>(sm, a, lane);
     return;
   }
   // consumers: ping-pong register buffers (the next stage is copied while this one is evaluated)
@@ -488,14 +499,14 @@ __global__ void __launch_bounds__(kThreads, 1) distance_st_kernel(DistArgs a) {
   // stage: its missing chunks are zero on both sides (target and source), adding nothing
   auto load = [&](uint4 (&dst)[KRE], int32_t bytes) {
     const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
-    if (!PARTIAL || bytes == StCfg<KRE>::kStageB) {     // exact geometries: no predicates at all
+    if (!PARTIAL || bytes == StCfg<KRE, CW>::kStageB) {   // exact geometries: no predicates at all
 #pragma unroll
-      for (int r = 0; r < KRE; ++r) dst[r] = src[tid + r * kConsumers];
+      for (int r = 0; r < KRE; ++r) dst[r] = src[tid + r * NC];
     } else {
       const int nchunk = bytes >> 4;
 #pragma unroll
       for (int r = 0; r < KRE; ++r) {
-        const int c = tid + r * kConsumers;
+        const int c = tid + r * NC;
         dst[r] = c < nchunk ? src[c] : make_uint4(0u, 0u, 0u, 0u);
       }
     }
@@ -538,10 +549,10 @@ __global__ void ticket_reset_kernel(unsigned int* ticket) {
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-__global__ void __launch_bounds__(kConsumers) finalize_kernel(DistArgs a, int from_partial) {
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(DistArgs a, int from_partial) {
   pdl_trigger();
   TL_SCOPE(7);
-  __shared__ double terms[kConsumers];
+  __shared__ double terms[kFinThreads];
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
   for (int64_t t = blockIdx.x; t < T; t += gridDim.x)
     finalize_target(a, t, terms, threadIdx.x, from_partial != 0, [] { __syncthreads(); });
@@ -560,7 +571,13 @@ static int st_maxk() {
   return v;
 }
 
-static int st_geometry(int64_t slice_bytes, int32_t* n_sub) {
+static int st_geometry(int64_t slice_bytes, int32_t* n_sub, int32_t* cw = nullptr) {
+  if (cw) *cw = kConsumerWarps;
+  if (slice_bytes == kPhi4Slice && st_maxk() >= 8) {   // one 40 KiB stage, ten consumer warps x 8 chunks
+    if (n_sub) *n_sub = 1;
+    if (cw) *cw = 10;
+    return 8;
+  }
   const int64_t units = (slice_bytes + kChunkUnit - 1) / kChunkUnit;
   const int maxk = st_maxk();
   const int64_t ns = (units + maxk - 1) / maxk;
@@ -569,18 +586,19 @@ static int st_geometry(int64_t slice_bytes, int32_t* n_sub) {
   return (int)(kre < 1 ? 1 : kre);
 }
 
-template <int KRE, int MET, bool PARTIAL>
+template <int KRE, int MET, bool PARTIAL, int CW = kConsumerWarps>
 static cudaError_t launch_st(const DistArgs& a, cudaStream_t st) {
   static bool attr_set_dev[kMaxDevices] = {};
   bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(distance_st_kernel<KRE, MET, PARTIAL>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(StSmem<KRE>));
+    const cudaError_t e = cudaFuncSetAttribute(distance_st_kernel<KRE, CW, MET, PARTIAL>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(StSmem<KRE, CW>));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_pdl(distance_st_kernel<KRE, MET, PARTIAL>, dim3(sm_count()), dim3(kThreads), sizeof(StSmem<KRE>),
-                    st, a);
+  return launch_pdl(distance_st_kernel<KRE, CW, MET, PARTIAL>, dim3(sm_count()), dim3(CW * 32 + 32),
+                    sizeof(StSmem<KRE, CW>), st, a);
 }
 
 // PARTIAL: the slice is not a whole number of stages (its last stage is partial); only those
@@ -603,6 +621,9 @@ static cudaError_t launch_st_kre(int kre, const DistArgs& a, cudaStream_t st) {
 }
 
 static cudaError_t launch_st_any(int kre, bool partial, int metric, const DistArgs& a, cudaStream_t st) {
+  if (a.cw == 10)                                       // the 40 KiB Phi-4 slice (exact: one stage)
+    return metric == MEMSHARE_METRIC_COSINE ? launch_st<8, MEMSHARE_METRIC_COSINE, false, 10>(a, st)
+                                            : launch_st<8, MEMSHARE_METRIC_EUCLIDEAN, false, 10>(a, st);
   if (metric == MEMSHARE_METRIC_COSINE)
     return partial ? launch_st_kre<MEMSHARE_METRIC_COSINE, true>(kre, a, st)
                    : launch_st_kre<MEMSHARE_METRIC_COSINE, false>(kre, a, st);
@@ -630,9 +651,10 @@ extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* di
   if (metric != MEMSHARE_METRIC_EUCLIDEAN && metric != MEMSHARE_METRIC_COSINE) return 0;
   const int64_t slice = (int64_t)dims->block_size * dims->num_kv_heads_local * dims->head_dim * 2;
   int32_t n_sub = 1;
-  st_geometry(slice, &n_sub);
+  int32_t cw = kConsumerWarps;
+  st_geometry(slice, &n_sub, &cw);
   Ws w{nullptr, 0};
-  dist_layout(w, dims->num_layers, n_sub, pair_cap, target_cap, metric);
+  dist_layout(w, dims->num_layers, n_sub, (cw + 3) / 4 * 4, pair_cap, target_cap, metric);
   return w.size();
 }
 
@@ -681,7 +703,8 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   a.num_blocks = num_blocks;
   a.N = dm.num_layers; a.d = dm.block_size; a.h_global = dm.num_kv_heads_global;
   a.slice_bytes = (int32_t)slice_bytes;
-  const int kre = st_geometry(slice_bytes, &a.n_sub);
+  const int kre = st_geometry(slice_bytes, &a.n_sub, &a.cw);
+  a.wstride = (a.cw + 3) / 4 * 4;
   static int lpi_env = -1;
   if (lpi_env < 0) {
     const char* e = getenv("MEMSHARE_LAYERS_PER_ITEM");
@@ -695,23 +718,23 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
   a.pair_cap = pair_cap; a.target_cap = target_cap; a.mode = mode; a.metric = metric; a.partial_sq = partial_sq; a.tau_b = tau_b;
   a.distance = distance; a.under = under; a.decisions = decisions; a.status = device_status;
   Ws w{static_cast<char*>(workspace), 0};
-  a.ws = dist_layout(w, a.N, a.n_sub, pair_cap, target_cap, metric);
+  a.ws = dist_layout(w, a.N, a.n_sub, a.wstride, pair_cap, target_cap, metric);
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t tc = target_cap < 1 ? 1 : target_cap;
   const int fin_grid = (int)(tc < 8 * sm_count() ? tc : 8 * sm_count());
   if (mode == MEMSHARE_DIST_FINALIZE) {
-    launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 1);
+    launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 1);
     return launch_status();
   }
   launch_pdl(ticket_reset_kernel, dim3(1), dim3(32), 0, st, a.ws.ticket);
   const bool prof = g_prof_begin != nullptr && g_prof_end != nullptr;
   if (prof && cudaEventRecord(g_prof_begin, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
-  const bool partial = slice_bytes % ((int64_t)kre * kChunkUnit) != 0;
+  const bool partial = slice_bytes % ((int64_t)kre * 16 * 32 * a.cw) != 0;
   const cudaError_t le = launch_st_any(kre, partial, metric, a, st);
   if (le != cudaSuccess) return MEMSHARE_ERR_CUDA;
   if (prof && cudaEventRecord(g_prof_end, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
-  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, st, a, 0);
+  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 0);
   return launch_status();
 }
 
@@ -736,17 +759,18 @@ extern "C" memshare_status memshare_block_distance_finalize_peers(
   a.N = dm.num_layers; a.d = dm.block_size; a.h_global = dm.num_kv_heads_global;
   const int64_t slice_bytes = (int64_t)dm.block_size * dm.num_kv_heads_local * dm.head_dim * 2;
   a.slice_bytes = (int32_t)slice_bytes;
-  st_geometry(slice_bytes, &a.n_sub);
+  st_geometry(slice_bytes, &a.n_sub, &a.cw);
+  a.wstride = (a.cw + 3) / 4 * 4;
   a.pairs = pairs; a.target_off = target_off; a.num_pairs = num_pairs; a.num_targets = num_targets;
   a.pair_cap = pair_cap; a.target_cap = target_cap; a.mode = MEMSHARE_DIST_FINALIZE;
   a.metric = MEMSHARE_METRIC_EUCLIDEAN; a.tau_b = tau_b;
   a.distance = distance; a.under = under; a.decisions = decisions; a.status = device_status;
   a.peers = partial_peers; a.num_peers = num_peers;
   Ws w{static_cast<char*>(workspace), 0};
-  a.ws = dist_layout(w, a.N, a.n_sub, pair_cap, target_cap, MEMSHARE_METRIC_EUCLIDEAN);
+  a.ws = dist_layout(w, a.N, a.n_sub, a.wstride, pair_cap, target_cap, MEMSHARE_METRIC_EUCLIDEAN);
   const int64_t tc = target_cap < 1 ? 1 : target_cap;
   const int fin_grid = (int)(tc < 8 * sm_count() ? tc : 8 * sm_count());
-  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kConsumers), 0, static_cast<cudaStream_t>(stream), a, 1);
+  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, static_cast<cudaStream_t>(stream), a, 1);
   return launch_status();
 }
 

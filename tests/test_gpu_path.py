@@ -212,10 +212,14 @@ def test_qwen32b_shape_two_sequences():
     full_parity(w)
 
 
-def test_phi4_shape_sub_slices():
-    """Phi-4's 40 KiB slice is streamed as two sub-slices (n_sub = 2)."""
+def test_phi4_shape_ten_consumer_warps():
+    """Phi-4's 40 KiB slice is one stage for ten consumer warps (8 chunks each); a 10-head slice of
+    head_dim 64 (20 KiB) and an 80 KiB slice (two 40 KiB stages, eight warps) around it."""
     w = workloads.small(kv.PHI4, 1, 3300, seed=5, gen_start=128, vocab=traces.PHI4_VOCAB)
     full_parity(w)
+    full_parity(w, tau_s=0.5, pairing=oracle.CROSS)
+    for shape in (kv.KVShape(2, 10, 64, 16), kv.KVShape(2, 10, 128, 32)):
+        full_parity(workloads.small(shape, 2, 1800, seed=6))
 
 
 @pytest.mark.parametrize("cur_mode", [oracle.CUR_ALL, oracle.CUR_LAST])
