@@ -78,6 +78,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-online", action="store_true")
+    ap.add_argument("--seed-sweep", default="0,1,2,3,4",
+                    help="c2: also time these seeds' pair lists (the paper's 5 runs) and report mean / min / max "
+                         "beside the --seed line ('' = off)")
     ap.add_argument("--breakdown", action="store_true", help="also time each ABI call separately (stderr)")
     ap.add_argument("--no-graph", action="store_true", help="launch the calls directly instead of CUDA-graph replay")
     a = ap.parse_args()
@@ -855,8 +858,33 @@ def run_single(args, rank, world, local):
         * args.steps,
         "clocks": ck, "e2e": e2e, "cpu_baseline": cpu, "online": online, "parity": parity,
     }
+    if args.config == "c2" and args.mode == "seq" and args.seed_sweep:
+        line["seed_stats"] = seed_sweep(args, dev, [int(x) for x in args.seed_sweep.split(",")], dist)
     line["roofline"]["kernel_share_of_step"] = d_ms / ms_step
     return line, dist, (parity is None or parity["ok"])
+
+
+def seed_sweep(args, dev, seeds, dist):
+    """The c2 step on other seeds' traces (five runs): pairs per second and the
+    distance call's fraction of the HBM peak per seed, and their mean / min / max. Each seed is a
+    different trace with a different amount of source sharing (192-622 pairs over 241-404 blocks)."""
+    from synth import workloads
+    per = []
+    for sd in seeds:
+        w = workloads.c2(seed=sd)
+        r = Run(w, dev, args, 1, 0, "seq", dist)
+        r.prepare()
+        alg, U, _ = r.alg_bytes()
+        clocks = ClockSampler(dev.index or 0)
+        ms, d_ms = r.timed(clocks)
+        clocks.stop()
+        per.append({"seed": sd, "pairs": r.counts["pairs"], "targets": r.counts["targets"], "distinct_blocks": U,
+                    "ms_per_step": ms, "pairs_per_s": r.counts["pairs"] / (ms / 1e3),
+                    "distance_frac": alg / (d_ms / 1e3) / 1e9 / measured_peaks()[0]})
+        r.free()
+    st = lambda k: {"mean": float(np.mean([x[k] for x in per])), "min": float(min(x[k] for x in per)),
+                    "max": float(max(x[k] for x in per))}
+    return {"seeds": seeds, "pairs_per_s": st("pairs_per_s"), "distance_frac": st("distance_frac"), "per_seed": per}
 
 
 # ----------------------------------------------------------------------------- our arm: a partitioned batch

@@ -148,9 +148,12 @@ typedef struct memshare_decision {
  *   step_nbag     int32 [step_cap]               content (non-delimiter) tokens of the step
  *   seq_step_off  int64 [num_seqs+1]             always written in full (the required size is
  *                                                seq_step_off[num_seqs]; CAPACITY if > step_cap)
- * Implementation: one single-pass kernel, tile-parallel over the flat token array (4096 tokens
- * per CTA) with a decoupled look-back scan of (step ends, content tokens, last step boundary),
- * so one long sequence spreads over many SMs (plus one memset of the per-tile flags).
+ * Implementation: one single-pass kernel, tile-parallel over the flat token array (2048 tokens
+ * per CTA, tiles handed out by an atomic ticket so a tile only waits on tiles already claimed by
+ * running CTAs) with a decoupled look-back scan of (step ends, content tokens, last step
+ * boundary), so one long sequence spreads over many SMs; a one-CTA kernel zeroes the per-tile
+ * flags and the ticket first (no memset node). A wait that does not end within 2 s reports
+ * CORRUPTION instead of hanging.
  * Errors: INVALID_ARGUMENT for null pointers, num_seqs < 0, num_delims outside 1..16, step_cap
  * < 0, a short workspace. */
 memshare_status memshare_segment_steps(const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off,
@@ -182,7 +185,11 @@ size_t memshare_segment_steps_workspace_size(int64_t num_tokens, int32_t num_seq
  *   target_off int64 [target_cap+1] (pairs of target t are [target_off[t], target_off[t+1]));
  *   num_matches/num_pairs/num_targets int64 (device).
  * Limits (CAPACITY if exceeded): <= 1024 survivors per current step when top_k == 0 or
- *   top_k > 512; <= 4096 full blocks per step. */
+ *   top_k > 512; <= 4096 full blocks per step.
+ * Implementation: current steps are work items taken from an atomic ticket (one CTA, or one
+ * thread-block cluster sharing the history scan over DSMEM in online LAST rounds); an item's output
+ * offsets are the sum of the counts every earlier item published, so it only ever waits on items
+ * running CTAs already hold (a wait beyond 2 s reports CORRUPTION). */
 memshare_status memshare_step_candidates(
     const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off, int32_t num_seqs,
     const int64_t* seq_step_off, const int32_t* step_start, const int32_t* step_end, const int32_t* step_nbag,
