@@ -53,12 +53,14 @@ BATCH_CONFIGS = ("c3", "c4", "c5")
 POOL_BUDGET = 140e9          # KV bytes one wave may take on a 180 GB B200 (the rest: workspaces, CUDA)
 
 
-def gpu_launches_per_step(num_tokens, sms=148):
-    """Our kernels per round: flag reset, seg, encode, stage1, (fill), ticket reset, distance,
-    finalize, remap. The library fuses the fill into stage1 for an offline round over at most
-    100 x 8 x SMs tokens (one CoT-sized batch); MEMSHARE_FUSED_FILL=0 disables it."""
+def gpu_launches_per_step(num_tokens, sms=148, fused_tail=True):
+    """Our kernels per round: flag reset, seg, encode, stage1, (fill), counter reset, distance
+    (+ finalize, remap unless a5-a7 is the fused memshare_block_distance_remap call, which
+    finalises and remaps inside the streaming kernel). The library fuses the fill into stage1 for
+    an offline round over at most 100 x 8 x SMs tokens (one CoT-sized batch);
+    MEMSHARE_FUSED_FILL=0 disables it."""
     fused = num_tokens <= 100 * 8 * sms and os.environ.get("MEMSHARE_FUSED_FILL", "1") != "0"
-    return 8 if fused else 9
+    return (6 if fused_tail else 8) + (0 if fused else 1)
 
 
 def parse():
@@ -391,6 +393,10 @@ class Run:
                 print(f"bench: symmetric memory unavailable ({e!r}); using the NCCL all-reduce", file=sys.stderr)
                 self.collective = "nccl"
         self.world = world
+        # a5-a6 (targets finalised inside the streaming kernel) then a7 as separate calls;
+        # MEMSHARE_BENCH_FUSED=1 times memshare_block_distance_remap (a5-a7 in one call: the remap in
+        # the streaming kernel's last CTA) -- measured ~4 us per round slower on B200
+        self.fused = mode != "headshard" and os.environ.get("MEMSHARE_BENCH_FUSED", "0") == "1"
         torch.cuda.synchronize()
         self.pristine = p.state.clone()
         self.stream = torch.cuda.current_stream(dev)
@@ -402,7 +408,11 @@ class Run:
         self.path.state.copy_(self.pristine, non_blocking=True)
 
     def distance(self):
+        """a5-a6 (a5-a7 when fused)."""
         p, L, w = self.path, self.L, self.w
+        if self.fused:
+            p.distance_remap(w.tau_b)
+            return
         if self.mode != "headshard":
             p.distance_call(w.tau_b)
             return
@@ -416,6 +426,11 @@ class Run:
                 self.dist.all_reduce(p.partial_sq[:self.counts["pairs"] * w.shape.num_layers * 2])
             p.distance_call(w.tau_b, L.DIST_FINALIZE)
 
+    def remap_phase(self):
+        """a7 (inside the a5-a7 call when fused)."""
+        if not self.fused:
+            self.path.remap()
+
     def prepare(self):
         p, w = self.path, self.w
 
@@ -424,21 +439,22 @@ class Run:
             p.segment()
             p.candidates(w.tau_s)
 
-        for fn in (front, self.distance, p.remap):     # eager warm-up (module load, attributes)
+        for fn in (front, self.distance, self.remap_phase):     # eager warm-up (module load, attributes)
             fn()
         self.torch.cuda.synchronize()
         if self.args.no_graph or self.collective != "none":    # collectives / symmetric-memory barriers: eager
-            self.run = (front, self.distance, p.remap)
+            self.run = (front, self.distance, self.remap_phase)
             self.full = None
         else:
             # the timed step: the whole round as ONE graph (a serving loop's replay); the a5-a6 timing
             # pass replays one graph per phase with events between them (graph boundaries cost ~4 us)
-            self.run = tuple(p.capture(fn).replay for fn in (front, self.distance, p.remap))
+            self.run = tuple(p.capture(fn).replay for fn in (front, self.distance)) + (
+                (lambda: None) if self.fused else p.capture(p.remap).replay,)
 
             def whole():
                 front()
                 self.distance()
-                p.remap()
+                self.remap_phase()
             self.full = p.capture(whole).replay
 
     def step(self, d_ev=None):
@@ -503,7 +519,7 @@ class Run:
         ks = []
         for i in range(n + 2):
             self.run[0]()
-            self.path.distance_call(self.w.tau_b)
+            self.distance()
             self.run[2]()
             self.torch.cuda.synchronize()
             if i >= 2:
@@ -528,8 +544,8 @@ class Run:
                 self.restore()
                 p.segment()
                 p.candidates(w.tau_s, cur_mode=cur_mode, cur_begin=cb, cur_end=ce)
-                p.distance_call(w.tau_b)
-                p.remap()
+                self.distance()
+                self.remap_phase()
             online_round()
             torch.cuda.synchronize()
             og = p.capture(online_round)
@@ -582,7 +598,7 @@ class Run:
                 p.segment()
                 p.candidates(w.tau_s)
                 self.distance()
-                p.remap()
+                self.remap_phase()
                 outs[j][0].copy_(p.outputs, non_blocking=True)
                 outs[j][1].copy_(p.state[:n_head], non_blocking=True)
             return body
@@ -760,10 +776,14 @@ def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_na
          "traffic": traffic, "kernel": kernel_name, "kernel_ms": d_ms, "algorithmic_bytes": alg_bytes,
          "pairs_per_s_a5a6": P / (d_ms / 1e3), "kv_bytes": kv_bytes, "distinct_blocks": U, "peak_source": peak_src,
          "frac_of_nominal_8000": achieved / 8000.0,
-         "note": "achieved/kernel_ms: CUDA events around the whole a5-a6 call (ticket reset + streaming kernel "
-                 "+ finalize, conservative) over K steps replayed phase by phase right after the timed loop (which "
-                 "replays each step as one graph); kernel_only_*: events around the streaming kernel alone "
-                 "(library profiling hook, eager calls)"}
+         "note": ("achieved/kernel_ms: CUDA events around the whole a5-a7 call (memshare_block_distance_remap: "
+                  "counter reset + streaming kernel with the finalisation and the remap fused in; conservative: the "
+                  "remap is inside)" if "remap" in kernel_name else
+                  "achieved/kernel_ms: CUDA events around the whole a5-a6 call (counter reset + streaming kernel, "
+                  "the targets finalised inside it; conservative)") +
+                 " over K steps replayed phase by phase right after the timed loop (which replays each step as one "
+                 "graph); kernel_only_*: events around the streaming kernel alone (library profiling hook, eager "
+                 "calls)"}
     if kernel_only_ms:
         r["kernel_only_ms"] = kernel_only_ms
         r["kernel_only_frac"] = alg_bytes / (kernel_only_ms / 1e3) / 1e9 / peak
@@ -851,11 +871,12 @@ def run_single(args, rank, world, local):
                             **({"collective": r.collective} if r.collective != "none" else {})}),
         "roofline": roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P,
                              committed_traffic(args.config, f"{args.config}_seed{args.seed}"),
-                             "distance_st_kernel (memshare_block_distance)"),
+                             "distance_st_kernel (memshare_block_distance_remap)" if r.fused
+                             else "distance_st_kernel (memshare_block_distance)"),
         "per_step": {"pairs": P, "targets": T, "steps": r.counts["steps"], "matches": r.counts["matches"],
                      "freed_blocks": step_freed, "affected_tokens": step_affected},
-        "gpu_launches": gpu_launches_per_step(w.num_tokens, torch.cuda.get_device_properties(dev).multi_processor_count)
-        * args.steps,
+        "gpu_launches": gpu_launches_per_step(w.num_tokens, torch.cuda.get_device_properties(dev).multi_processor_count,
+                                              r.fused) * args.steps,
         "clocks": ck, "e2e": e2e, "cpu_baseline": cpu, "online": online, "parity": parity,
     }
     if args.config == "c2" and args.mode == "seq" and args.seed_sweep:
@@ -958,13 +979,14 @@ def run_batch(args, rank, world, local):
     waves, ms_step, e_ms, parity_ok = [], 0.0, 0.0, True
     tot = {"pairs": 0, "targets": 0, "steps": 0, "matches": 0, "alg": 0, "kv": 0, "U": 0, "d_ms": 0.0, "k_ms": 0.0,
            "freed": 0, "affected": 0, "tokens": 0, "h2d": 0, "d2h": 0, "launches": 0}
-    online, first_w = None, None
+    online, first_w, fused_tail = None, None, True
     for wi, idx in enumerate(my_waves):
         if not idx:
             continue
         w = workloads.batch(cfg, idx, args.seed)
         first_w = first_w or w
         r = Run(w, dev, args, world, rank, "seq", dist)
+        fused_tail = r.fused
         r.prepare()
         alg, U, kvb = r.alg_bytes()
         m, d_ms = r.timed(clocks)
@@ -986,7 +1008,8 @@ def run_batch(args, rank, world, local):
                        ("matches", c["matches"]), ("alg", alg), ("kv", kvb), ("U", U), ("d_ms", d_ms),
                        ("k_ms", k_ms), ("freed", freed), ("affected", affected), ("tokens", w.num_tokens),
                        ("launches", gpu_launches_per_step(w.num_tokens,
-                                                          torch.cuda.get_device_properties(dev).multi_processor_count))):
+                                                          torch.cuda.get_device_properties(dev).multi_processor_count,
+                                                          r.fused))):
             tot[k_] += v_
         waves.append({"rank": rank, "wave": wi, "seqs": len(idx), "tokens": w.num_tokens, "pairs": c["pairs"],
                       "targets": c["targets"], "distinct_blocks": U, "ms_per_step": m, "distance_ms": d_ms,
@@ -1032,7 +1055,8 @@ def run_batch(args, rank, world, local):
                             "plan_s": round(t_plan, 2), "baseline_config": f"configs[{ci}]"}),
         "roofline": roofline(tot["alg"], tot["d_ms"], tot["k_ms"], tot["kv"], tot["U"], tot["pairs"],
                              committed_traffic(cfg, f"{cfg}_{n}seq_{world}gpu_seed{args.seed}"),
-                             "distance_st_kernel (memshare_block_distance)"),
+                             "distance_st_kernel (memshare_block_distance_remap)" if fused_tail
+                             else "distance_st_kernel (memshare_block_distance)"),
         "per_step": {"pairs": int(pairs_all), "pairs_rank0": tot["pairs"], "targets_rank0": tot["targets"],
                      "steps_rank0": tot["steps"], "matches_rank0": tot["matches"], "freed_blocks_rank0": tot["freed"],
                      "affected_tokens_rank0": tot["affected"]},

@@ -252,6 +252,29 @@ memshare_status memshare_remap(int32_t* block_table, int32_t table_stride, int32
                                size_t workspace_bytes, int32_t* device_status, void* stream);
 size_t memshare_remap_workspace_size(int32_t num_blocks, int64_t target_cap);
 
+/* ------------------------------------------------------------------------------------- a5-a7
+ * memshare_block_distance (FULL mode) and memshare_remap as ONE call, for a round that applies its
+ * decisions at once (score, select, then "the block table is updated",
+ * PAPER.md:276-278). Results are identical to memshare_block_distance(mode = FULL) followed by
+ * memshare_remap on the same stream: the same distances, under flags and decisions (bit for bit),
+ * the same table / refcount / free-list update and counters, the same device errors (a remap
+ * validation failure changes nothing). Arguments are those of the two calls; num_blocks is
+ * pool_host->num_blocks; partial_sq is not produced.
+ *   workspace >= memshare_block_distance_remap_workspace_size() bytes.
+ * Implementation: every target is finalised inside the streaming kernel by the consumer warp that
+ * completes its last (target, layer chunk) unit (per-target completion counts), and the last CTA of
+ * the streaming kernel to finish applies the decisions -- two launches (counter reset, stream)
+ * instead of four. Errors: as memshare_block_distance and memshare_remap. */
+memshare_status memshare_block_distance_remap(
+    const memshare_kv_pool* pool_host, const memshare_dims* dims_host, const memshare_block_pair* pairs,
+    const int64_t* target_off, const int64_t* num_pairs, const int64_t* num_targets, int64_t pair_cap,
+    int64_t target_cap, int32_t metric, float tau_b, float* distance, uint8_t* under, memshare_decision* decisions,
+    int32_t* block_table, int32_t table_stride, int32_t num_seqs, int32_t* refcount, int32_t* free_list,
+    int64_t* free_count, int32_t block_size, int64_t* num_freed, int64_t* affected_tokens, void* workspace,
+    size_t workspace_bytes, int32_t* device_status, void* stream);
+size_t memshare_block_distance_remap_workspace_size(const memshare_dims* dims_host, int32_t num_blocks,
+                                                    int64_t pair_cap, int64_t target_cap, int32_t metric);
+
 /* ---------------------------------------------------------------------------------------- f4
  * Similarity ratio (Fig. 2: "the proportion of reasoning steps whose cosine
  * similarity with any previous step exceeds a specified threshold"). From memshare_step_candidates'

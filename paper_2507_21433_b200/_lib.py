@@ -64,6 +64,11 @@ def _load():
     L.memshare_block_distance.restype = I32
     L.memshare_block_distance_workspace_size.argtypes = [P, I32, I64, I64, I32]
     L.memshare_block_distance_workspace_size.restype = U64
+    L.memshare_block_distance_remap.argtypes = [P, P, P, P, P, P, I64, I64, I32, F32, P, P, P, P, I32, I32, P, P, P, I32,
+                                                P, P, P, U64, P, P]
+    L.memshare_block_distance_remap.restype = I32
+    L.memshare_block_distance_remap_workspace_size.argtypes = [P, I32, I64, I64, I32]
+    L.memshare_block_distance_remap_workspace_size.restype = U64
     L.memshare_block_distance_finalize_peers.argtypes = [P, I32, P, P, P, P, P, I64, I64, F32, P, P, P, P, U64, P, P]
     L.memshare_block_distance_finalize_peers.restype = I32
     L.memshare_remap.argtypes = [P, I32, I32, P, I32, P, P, P, P, I64, I32, P, P, P, U64, P, P]
@@ -177,6 +182,26 @@ def block_distance(pool: KVPool | None, dims: Dims, pairs, target_off, num_pairs
         None if pool is None else ctypes.byref(pool), ctypes.byref(dims), _ptr(pairs), _ptr(target_off),
         _ptr(num_pairs), _ptr(num_targets), pair_cap, target_cap, mode, metric, _ptr(partial_sq), float(tau_b),
         _ptr(distance), _ptr(under), _ptr(decisions), _ptr(workspace),
+        0 if workspace is None else workspace.numel() * workspace.element_size(), _ptr(device_status),
+        _stream(stream))
+
+
+def block_distance_remap_workspace_size(dims: Dims, num_blocks: int, pair_cap: int, target_cap: int,
+                                        metric: int = METRIC_EUCLIDEAN) -> int:
+    return lib.memshare_block_distance_remap_workspace_size(ctypes.byref(dims), num_blocks, pair_cap, target_cap,
+                                                            metric)
+
+
+def block_distance_remap(pool: KVPool, dims: Dims, pairs, target_off, num_pairs, num_targets, pair_cap, target_cap,
+                         metric, tau_b, distance, under, decisions, block_table, table_stride, num_seqs, refcount,
+                         free_list, free_count, block_size, num_freed, affected_tokens, workspace, device_status,
+                         stream=None) -> int:
+    """a5-a7 in one call (memshare_block_distance FULL + memshare_remap)."""
+    return lib.memshare_block_distance_remap(
+        ctypes.byref(pool), ctypes.byref(dims), _ptr(pairs), _ptr(target_off), _ptr(num_pairs), _ptr(num_targets),
+        pair_cap, target_cap, metric, float(tau_b), _ptr(distance), _ptr(under), _ptr(decisions), _ptr(block_table),
+        table_stride, num_seqs, _ptr(refcount), _ptr(free_list), _ptr(free_count), block_size, _ptr(num_freed),
+        _ptr(affected_tokens), _ptr(workspace),
         0 if workspace is None else workspace.numel() * workspace.element_size(), _ptr(device_status),
         _stream(stream))
 

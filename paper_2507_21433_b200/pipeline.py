@@ -149,7 +149,9 @@ class MemSharePath:
                  L.step_candidates_workspace_size(self.num_tokens, self.num_seqs, caps.step, caps.match),
                  L.block_distance_workspace_size(self.dims, self.num_blocks, caps.pair, caps.target,
                                                  L.METRIC_COSINE),
-                 L.remap_workspace_size(self.num_blocks, caps.target))
+                 L.remap_workspace_size(self.num_blocks, caps.target),
+                 L.block_distance_remap_workspace_size(self.dims, self.num_blocks, caps.pair, caps.target,
+                                                       L.METRIC_COSINE))
         self.workspace = e(ws, torch.uint8)
 
     def alloc_partial(self):
@@ -193,6 +195,16 @@ class MemSharePath:
         L.check(L.remap(self.table, self.table_stride, self.num_seqs, self.refcount, self.num_blocks, self.free_list,
                         self.free_count, self.decisions, self.num_targets, self.caps.target, self.block_size,
                         self.num_freed, self.affected, self.workspace, self.status, self.stream), "remap")
+
+    def distance_remap(self, tau_b, metric=L.METRIC_EUCLIDEAN):
+        """a5-a7 as one call: distance_call(FULL) + remap() with the finalisation and the remap fused
+        into the streaming kernel (identical results)."""
+        L.check(L.block_distance_remap(self.pool, self.dims, self.pairs, self.target_off, self.num_pairs,
+                                       self.num_targets, self.caps.pair, self.caps.target, metric, tau_b,
+                                       self.distance, self.under, self.decisions, self.table, self.table_stride,
+                                       self.num_seqs, self.refcount, self.free_list, self.free_count,
+                                       self.block_size, self.num_freed, self.affected, self.workspace, self.status,
+                                       self.stream), "block_distance_remap")
 
     # ------------------------------------------------------------------ analysis (f3, f4)
     def similarity_ratio(self):

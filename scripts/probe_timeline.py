@@ -49,7 +49,10 @@ def show(title, tl, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--separate", action="store_true", help="a5-a7 as block_distance + remap (default: fused call)")
     args = ap.parse_args()
+    if args.separate:
+        os.environ["MEMSHARE_BENCH_FUSED"] = "0"
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     ns = argparse.Namespace(collective="nccl", no_graph=False, steps=1, warmup=3)
@@ -57,20 +60,20 @@ def main():
     r = bench.Run(w, dev, ns)
     r.prepare()
     for _ in range(5):
-        r.step()
+        r.full()
     torch.cuda.synchronize()
     read(True)
-    r.step()
+    r.full()
     torch.cuda.synchronize()
-    show("offline c2 step (graph replay of front / a5-a6 / a7)", read(True), 1)
+    show("offline c2 step (one graph)", read(True), 1)
     p = r.path
 
     def online():
         r.restore()
         p.segment()
         p.candidates(w.tau_s, cur_mode=L.CUR_LAST)
-        p.distance_call(w.tau_b)
-        p.remap()
+        r.distance()
+        r.remap_phase()
     online()
     torch.cuda.synchronize()
     g = p.capture(online)

@@ -28,13 +28,20 @@ def _cuda():
     build.build()
 
 
-def full_parity(w, tau_s=None, tau_b=None, top_k=0, pairing=oracle.ALIGNED, cur_mode=oracle.CUR_ALL, cb=None, ce=None):
+def full_parity(w, tau_s=None, tau_b=None, top_k=0, pairing=oracle.ALIGNED, cur_mode=oracle.CUR_ALL, cb=None, ce=None,
+                fused=False):
+    """One round through the four calls (fused=True: a5-a7 through memshare_block_distance_remap)."""
     import torch
     p = make_path(w)
     tau_s = w.tau_s if tau_s is None else tau_s
     tau_b = w.tau_b if tau_b is None else tau_b
     p.autosize(tau_s, top_k, pairing, cur_mode, cb, ce)
-    p.round(tau_s, tau_b, top_k, pairing, cur_mode, cb, ce)
+    if fused:
+        p.segment()
+        p.candidates(tau_s, top_k, pairing, cur_mode, cb, ce)
+        p.distance_remap(tau_b)
+    else:
+        p.round(tau_s, tau_b, top_k, pairing, cur_mode, cb, ce)
     torch.cuda.synchronize()
     return check_round(p, w, tau_s, tau_b, top_k, pairing, cur_mode, cb, ce)
 
@@ -177,9 +184,11 @@ def test_randomized_configurations(seed):
     if mode == 2:
         cb = [int(x) for x in rng.integers(0, 6, num_seqs)]
         ce = [b + int(x) for b, x in zip(cb, rng.integers(1, 12, num_seqs))]
-        full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=oracle.CUR_RANGE, cb=cb, ce=ce)
+        full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=oracle.CUR_RANGE, cb=cb, ce=ce,
+                    fused=seed % 2 == 1)
     else:
-        full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=[oracle.CUR_ALL, oracle.CUR_LAST][mode])
+        full_parity(w, tau_s=tau_s, top_k=top_k, pairing=pairing, cur_mode=[oracle.CUR_ALL, oracle.CUR_LAST][mode],
+                    fused=seed % 2 == 1)
 
 
 @pytest.mark.parametrize("shape", [kv.KVShape(2, 3, 64, 16), kv.KVShape(2, 12, 128, 16), kv.KVShape(2, 20, 128, 16),
@@ -250,6 +259,88 @@ def test_bit_reproducible_rounds(cur_mode):
         assert np.array_equal(d0["decisions"][k], d1["decisions"][k]), k
     for k in ("table", "refcount", "free_list"):
         assert np.array_equal(s0[k], s1[k]), k
+
+
+def _round_outputs(p):
+    c, d, st = p.read_candidates(), p.read_distance(), p.read_state()
+    return c, d, st
+
+
+@pytest.mark.parametrize("case", ["tiny0", "tiny5", "chain", "small", "cross", "phi4", "geom", "two_rounds"])
+def test_fused_distance_remap_matches_separate_calls(case):
+    """memshare_block_distance_remap (a5-a7 in one call: targets finalised inside the streaming
+    kernel by a finaliser warp, the remap run by the streaming kernel's last CTA) against
+    memshare_block_distance + memshare_remap on the same round: distances, under flags, decisions,
+    table, refcounts, free list and counters bit-identical, and the fused round passes the full
+    oracle check."""
+    import torch
+    tau_s, pairing, rounds = None, oracle.ALIGNED, 1
+    if case in ("tiny0", "tiny5"):
+        w = workloads.tiny(eta=0.0 if case == "tiny0" else 0.05)
+    elif case == "chain":
+        w = _t1_chain_workload(extra_copies=5)
+    elif case == "small":
+        w = workloads.small(SMALL, 3, 2500, seed=3)
+    elif case == "cross":
+        w, tau_s, pairing = workloads.small(SMALL, 2, 2500, seed=7), 0.3, oracle.CROSS
+    elif case == "phi4":
+        w = workloads.small(kv.PHI4, 1, 3300, seed=5, gen_start=128, vocab=traces.PHI4_VOCAB)
+    elif case == "geom":
+        w, tau_s, pairing = workloads.small(kv.KVShape(2, 3, 64, 16), 2, 1800, seed=3), 0.6, oracle.CROSS
+    else:
+        w, rounds = workloads.small(SMALL, 2, 2500, seed=11, eta=0.0), 2
+    tau_s = w.tau_s if tau_s is None else tau_s
+    tau_b = 1e-3 if case == "two_rounds" else w.tau_b
+    outs = []
+    for fused in (False, True):
+        p = make_path(w)
+        p.autosize(tau_s, pairing=pairing)
+        for _ in range(rounds):
+            p.segment()
+            p.candidates(tau_s, pairing=pairing)
+            if fused:
+                p.distance_remap(tau_b)
+            else:
+                p.distance_call(tau_b)
+                p.remap()
+        torch.cuda.synchronize()
+        assert p.read_status() == 0
+        outs.append(_round_outputs(p))
+        if fused and rounds == 1:
+            check_round(p, w, tau_s, tau_b, pairing=pairing)
+        del p
+    (c0, d0, s0), (c1, d1, s1) = outs
+    assert c0["pairs"]["seq"].size > 0
+    assert np.array_equal(d0["distance"].view(np.uint32), d1["distance"].view(np.uint32))
+    assert np.array_equal(d0["under"], d1["under"])
+    for k in d0["decisions"]:
+        assert np.array_equal(d0["decisions"][k], d1["decisions"][k]), k
+    for k in ("table", "refcount", "free_list", "free_count", "num_freed", "affected"):
+        assert np.array_equal(s0[k], s1[k]), k
+
+
+def test_fused_distance_remap_rejects_bad_decisions_like_remap():
+    """A remap validation failure in the fused call changes nothing (as memshare_remap): a
+    corrupted block table entry makes the fused call report CORRUPTION and leave the state."""
+    import torch
+    w = workloads.small(SMALL, 2, 2500, seed=3)
+    p = make_path(w)
+    p.autosize(w.tau_s)
+    p.segment()
+    p.candidates(w.tau_s)
+    torch.cuda.synchronize()
+    d = p.read_candidates()
+    tgt = d["pairs"]
+    assert tgt["seq"].size > 0
+    s, tl = int(tgt["seq"][0]), int(tgt["target_logical"][0])
+    p.table.view(p.num_seqs, p.table_stride)[s, tl] = p.num_blocks + 5     # out of range: CORRUPTION
+    before = p.read_state()
+    p.distance_remap(1e9)                                                   # every decision accepted
+    torch.cuda.synchronize()
+    assert p.read_status() == 3
+    after = p.read_state()
+    for k in ("table", "refcount", "free_list"):
+        assert np.array_equal(before[k], after[k]), k
 
 
 @pytest.mark.parametrize("pairing,tau_s", [(oracle.ALIGNED, 0.5), (oracle.CROSS, 0.3)])
