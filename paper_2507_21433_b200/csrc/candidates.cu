@@ -256,14 +256,16 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
 // step's private region of the global workspace; n2 = sum of count^2 (int64, exact).
 constexpr int kEncSlots = kSmemSlots / kNW;                // 1024 slots per warp
 
+template <int kSlotsW = kEncSlots>
 __device__ int64_t warp_step_n2(const CandArgs& a, int2* s_tab, const int32_t* t, int64_t tok_base, int32_t start,
                                 int32_t end, int32_t nbag) {
   const int lane = threadIdx.x & 31;
   int2* slots;
   uint32_t cap;
   bool global;
-  if (nbag <= kEncSlots / 4) {
+  if (nbag <= kSlotsW / 2) {                          // load factor <= 0.5 (<= 0.25 when the slots allow)
     cap = pow2_ceil(4u * (uint32_t)(nbag > 32 ? nbag : 32));
+    if (cap > (uint32_t)kSlotsW) cap = (uint32_t)kSlotsW;
     slots = s_tab;
     global = false;
   } else {
@@ -748,6 +750,225 @@ __device__ void s1_totals(const CandArgs& a, int4 incl) {
   }
 }
 
+
+// Publish "no outputs" for work item `key` of the fused fill (all CTA threads call it; the last key
+// also writes the totals).
+template <int NT>
+__device__ void s1_publish_nothing(const CandArgs& a, int64_t key, int64_t nwork, int4* s_lb) {
+  if (key == nwork - 1) {
+    const int4 pre = s1_prefix(a, key, 0, 0, 0, s_lb);
+    s1_totals(a, pre);
+  } else if (threadIdx.x == 0) {
+    s1_st_relaxed(a.ws.lb_agg + key, make_int4(1, 1, 1, 1));
+  }
+}
+
+// One Stage-1 work item: current step g (local k) of sequence s (steps [gfirst, gfirst + S)):
+// table, history stream (this CTA's share of a cluster's), selection, pair counts and -- fused --
+// the fill. All threads of the CTA (and of its cluster) call it.
+template <int NT>
+__device__ void s1_item(const CandArgs& a, SelSmem<NT>& sm, int64_t wi, int64_t g, int32_t s, int64_t gfirst,
+                        int64_t S, bool fused, int64_t nwork, int4* s_lb_p) {
+  constexpr int kNTs = NT, kNWs = NT / 32;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int csize = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int4& s_lb = *s_lb_p;
+  auto publish_nothing = [&](int64_t key) { s1_publish_nothing<NT>(a, key, nwork, s_lb_p); };
+  const int64_t k = g - gfirst;
+  const int32_t nbag = a.step_nbag[g];
+  if (nbag == 0 || !is_current(a, s, k, S)) {
+    if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
+    if (fused && crank == 0) publish_nothing(wi);
+    return;
+  }
+  const int64_t tok_base = a.seq_tok_off[s];
+  const int32_t* t = a.tokens + tok_base;
+  const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots,
+                               sm.u.bm, crank == 0);
+  if (tb.global && csize > 1) cl.sync();                 // rank 0 filled the shared global table
+  DBG_T(1);
+  const double n2k = (double)a.ws.n2[g];
+  if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
+  __syncthreads();
+  const bool compact = a.top_k > 0 && a.top_k <= kCandCap / 2;
+  // The history of step k is the contiguous token range [start_0, end_{k-1}) of the sequence:
+  // stream it with all threads (coalesced), look each content token up in k's table and add
+  // the count to the dot product of the step that holds it (smem atomics, only for hits).
+  for (int64_t jb = 0; jb < k; jb += kChunk) {
+    const int64_t je = (jb + kChunk < k) ? jb + kChunk : k;
+    const int nj = (int)(je - jb);
+    for (int i = threadIdx.x; i < nj; i += kNTs) {
+      sm.hst[i] = a.step_start[gfirst + jb + i];
+      sm.hen[i] = a.step_end[gfirst + jb + i];
+      sm.dot_lo[i] = 0u;
+      sm.dot_hi[i] = 0u;
+    }
+    __syncthreads();
+    if (jb == 0) DBG_T(10);
+    if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
+      g_dbg_t[blockIdx.x * kDbgSlots + 12] = clock64();
+    const int32_t lo0 = sm.hst[0], hi0 = sm.hen[nj - 1];
+    const int32_t lo = lo0 + (int32_t)((int64_t)(hi0 - lo0) * crank / csize);      // this rank's share
+    const int32_t hi = lo0 + (int32_t)((int64_t)(hi0 - lo0) * (crank + 1) / csize);
+    for (int32_t clo = lo; clo < hi; clo += S1Cfg<NT>::kTok) {
+      const int32_t chi = (hi - clo > S1Cfg<NT>::kTok) ? clo + S1Cfg<NT>::kTok : hi;
+      // coalesced, independent loads: one memory latency for the whole pass
+#pragma unroll 4
+      for (int32_t i = threadIdx.x; i < chi - clo; i += kNTs) sm.tok[i] = __ldg(t + clo + i);
+      __syncthreads();
+      if (jb == 0 && clo == lo) DBG_T(14);
+      if (!(a.dbg_skip & 1)) {
+        if (tb.global)
+          stream_history<true>(tb.slots, sm.u.bm, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
+                               a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
+        else
+          stream_history<false>(sm.tab, sm.u.bm, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
+                                a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (csize > 1) {
+      cl.sync();                                         // every rank's partial dots are final
+      if (crank == 0) {
+        // every remote load issued before any sum (one DSMEM latency, not csize - 1 of them)
+        for (int i = threadIdx.x; i < nj; i += kNTs) {
+          uint32_t lo_r[8], hi_r[8];
+#pragma unroll
+          for (int r = 1; r < 8; ++r) {
+            lo_r[r] = r < csize ? cl.map_shared_rank(sm.dot_lo, r)[i] : 0u;
+            hi_r[r] = r < csize ? cl.map_shared_rank(sm.dot_hi, r)[i] : 0u;
+          }
+          uint64_t d = ((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i];
+#pragma unroll
+          for (int r = 1; r < 8; ++r) d += ((uint64_t)hi_r[r] << 32) | lo_r[r];
+          sm.dot_lo[i] = (uint32_t)d;
+          sm.dot_hi[i] = (uint32_t)(d >> 32);
+        }
+      }
+      cl.sync();                                         // remote reads done before ranks reuse them
+      if (crank != 0) continue;                          // ranks > 0 only stream (uniform per CTA)
+    }
+    if (jb == 0) DBG_T(11);
+    if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
+      g_dbg_t[blockIdx.x * kDbgSlots + 13] = clock64();
+    for (int i = threadIdx.x; i < nj; i += kNTs) {
+      const int64_t gj = gfirst + jb + i;
+      if (a.step_nbag[gj] == 0) continue;                // void history step (reading R5)
+      const int64_t dot = (int64_t)(((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i]);
+      // sim = <v_curr, v_i> / (||v_curr|| ||v_i||), reading R12
+      const double cs = __ddiv_rn(__ll2double_rn(dot), __dsqrt_rn(__dmul_rn(n2k, __ll2double_rn(a.ws.n2[gj]))));
+      if (cs > a.tau_s) {                                // strict: "exceeding"
+        const int idx = atomicAdd(&sm.count, 1);
+        if (idx < kCandCap) { sm.cs[idx] = cs; sm.js[idx] = (int32_t)(jb + i); }
+        else sm.overflow = 1;
+      }
+    }
+    __syncthreads();
+    if (compact && sm.count > kCandCap / 2) {
+      sort_cands(sm.cs, sm.js, sm.count);
+      __syncthreads();
+      if (threadIdx.x == 0) sm.count = a.top_k;
+      __syncthreads();
+    }
+  }
+  if (crank != 0) return;
+  DBG_T(2);
+  if (sm.overflow) {
+    if (threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+    __syncthreads();
+  }
+  int m = sm.count < kCandCap ? sm.count : kCandCap;
+  sort_cands(sm.cs, sm.js, m);
+  if (a.top_k > 0 && m > a.top_k) m = a.top_k;
+  DBG_T(3);
+  // stash the ranked survivors for the fill kernel
+  __shared__ unsigned long long s_base;
+  if (threadIdx.x == 0) {
+    s_base = (m > 0 && !fused) ? atomicAdd(a.ws.stash_alloc, (unsigned long long)m) : 0ull;
+    if (!fused && (int64_t)(s_base + m) > a.match_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)s_base;
+  for (int r = threadIdx.x; r < m; r += kNTs) {
+    if (!fused && base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
+    sm.u.l.jasc[r] = sm.js[r];
+  }
+  if (threadIdx.x == 0) { sm.acc_t = 0u; sm.acc_p = 0u; }
+  __syncthreads();
+  // a4: count targets and deduplicated pairs of this step
+  DBG_T(4);
+  Cands c{m, sm.u.l.jasc, sm.u.l.flo, sm.flen, sm.cum};
+  prepare_cands(a, c, gfirst);
+  DBG_T(5);
+  const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
+  const int32_t nt = (m > 0 && fk_hi > fk_lo) ? fk_hi - fk_lo : 0;
+  if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
+  const int32_t* trow = a.table + (int64_t)s * a.table_stride;
+  int64_t my_t = 0, my_p = 0;
+  // fused fill: the history staging area is free now; it holds the per-target kept counts,
+  // pair offsets and target numbers of the step (kMaxTgt x 16 B = 64 KiB)
+  int32_t* f_tc = reinterpret_cast<int32_t*>(sm.tok);
+  int64_t* f_tpos = reinterpret_cast<int64_t*>(f_tc + kMaxTgt);
+  int32_t* f_tnum = reinterpret_cast<int32_t*>(f_tpos + kMaxTgt);
+  for (int32_t i = w; i < nt && !(a.dbg_skip & 2); i += kNWs) {
+    const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
+    my_t += kept > 0 ? 1 : 0;
+    my_p += kept;
+    if (fused && lane == 0 && i < kMaxTgt) f_tc[i] = kept;
+  }
+  if (lane == 0) { atomicAdd(&sm.acc_t, (uint32_t)my_t); atomicAdd(&sm.acc_p, (uint32_t)my_p); }
+  __syncthreads();
+  DBG_T(6);
+  if (threadIdx.x == 0) {
+    a.ws.cnt_m[g] = m;
+    a.ws.cnt_t[g] = (int32_t)sm.acc_t;
+    a.ws.cnt_p[g] = (int32_t)sm.acc_p;
+    a.ws.stash_base[g] = base;
+  }
+  __syncthreads();
+  if (fused) {
+    // offsets of this step's outputs, then the fill kernel's work done here
+    const int4 pre = s1_prefix(a, wi, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
+    DBG_T(8);
+    if (wi == nwork - 1) s1_totals(a, make_int4(pre.x + m, pre.y + (int32_t)sm.acc_t, pre.z + (int32_t)sm.acc_p, 0));
+    const int64_t mo = pre.x, to = pre.y, po = pre.z;
+    for (int r = threadIdx.x; r < m; r += kNTs) {
+      if (mo + r < a.match_cap) {
+        memshare_step_match mt;
+        mt.seq = s; mt.step = (int32_t)k; mt.cand_step = sm.js[r]; mt.rank = r; mt.cosine = sm.cs[r];
+        a.matches[mo + r] = mt;
+      }
+    }
+    const int32_t ntf = nt < kMaxTgt ? nt : kMaxTgt;
+    int64_t pcarry = 0, tcarry = 0;
+    for (int32_t ib = 0; ib < ntf; ib += kNTs) {
+      const int32_t i = ib + threadIdx.x;
+      const int64_t v = i < ntf ? f_tc[i] : 0;
+      int64_t tot;
+      const int64_t ex = block_excl_scan<NT>(v, tot, sm.sh);
+      int64_t tt;
+      const int64_t tex = block_excl_scan<NT>(v > 0 ? 1 : 0, tt, sm.sh);
+      if (i < ntf) { f_tpos[i] = pcarry + ex; f_tnum[i] = v > 0 ? (int32_t)(tcarry + tex) : -1; }
+      pcarry += tot;
+      tcarry += tt;
+    }
+    __syncthreads();
+    DBG_T(9);
+    for (int32_t i = w; i < ntf; i += kNWs) {
+      if (f_tnum[i] < 0) continue;
+      const int64_t tidx = to + f_tnum[i];
+      const int32_t tl = fk_lo + i;
+      const int32_t tphys = phys_of(a, trow, tl);
+      target_sources(a, c, trow, s, i, tl, tphys, (int32_t)tidx, a.pairs, po + f_tpos[i], a.pair_cap);
+      if (lane == 0 && tidx < a.target_cap) a.target_off[tidx] = po + f_tpos[i];
+    }
+    __syncthreads();
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   constexpr int kNTs = NT, kNWs = NT / 32;
@@ -820,193 +1041,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
     const int32_t s = a.ws.step_seq[g];
     const int64_t gfirst = a.seq_step_off[s];
     const int64_t S = a.seq_step_off[s + 1] - gfirst;
-    const int64_t k = g - gfirst;
-    const int32_t nbag = a.step_nbag[g];
-    if (nbag == 0 || !is_current(a, s, k, S)) {
-      if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
-      if (fused && crank == 0) publish_nothing(wi);
-      continue;
-    }
-    const int64_t tok_base = a.seq_tok_off[s];
-    const int32_t* t = a.tokens + tok_base;
-    const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots,
-                                 sm.u.bm, crank == 0);
-    if (tb.global && csize > 1) cl.sync();                 // rank 0 filled the shared global table
-    DBG_T(1);
-    const double n2k = (double)a.ws.n2[g];
-    if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
-    __syncthreads();
-    const bool compact = a.top_k > 0 && a.top_k <= kCandCap / 2;
-    // The history of step k is the contiguous token range [start_0, end_{k-1}) of the sequence:
-    // stream it with all threads (coalesced), look each content token up in k's table and add
-    // the count to the dot product of the step that holds it (smem atomics, only for hits).
-    for (int64_t jb = 0; jb < k; jb += kChunk) {
-      const int64_t je = (jb + kChunk < k) ? jb + kChunk : k;
-      const int nj = (int)(je - jb);
-      for (int i = threadIdx.x; i < nj; i += kNTs) {
-        sm.hst[i] = a.step_start[gfirst + jb + i];
-        sm.hen[i] = a.step_end[gfirst + jb + i];
-        sm.dot_lo[i] = 0u;
-        sm.dot_hi[i] = 0u;
-      }
-      __syncthreads();
-      if (jb == 0) DBG_T(10);
-      if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
-        g_dbg_t[blockIdx.x * kDbgSlots + 12] = clock64();
-      const int32_t lo0 = sm.hst[0], hi0 = sm.hen[nj - 1];
-      const int32_t lo = lo0 + (int32_t)((int64_t)(hi0 - lo0) * crank / csize);      // this rank's share
-      const int32_t hi = lo0 + (int32_t)((int64_t)(hi0 - lo0) * (crank + 1) / csize);
-      for (int32_t clo = lo; clo < hi; clo += S1Cfg<NT>::kTok) {
-        const int32_t chi = (hi - clo > S1Cfg<NT>::kTok) ? clo + S1Cfg<NT>::kTok : hi;
-        // coalesced, independent loads: one memory latency for the whole pass
-#pragma unroll 4
-        for (int32_t i = threadIdx.x; i < chi - clo; i += kNTs) sm.tok[i] = __ldg(t + clo + i);
-        __syncthreads();
-        if (jb == 0 && clo == lo) DBG_T(14);
-        if (!(a.dbg_skip & 1)) {
-          if (tb.global)
-            stream_history<true>(tb.slots, sm.u.bm, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
-                                 a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
-          else
-            stream_history<false>(sm.tab, sm.u.bm, tb.mask, tb.shift, sm.dot_lo, sm.dot_hi, sm.hen, nj, a.dl.id[0], a.dl.n,
-                                  a.dl, sm.tok, clo, chi, (a.dbg_skip & 16) != 0);
-        }
-        __syncthreads();
-      }
-      __syncthreads();
-      if (csize > 1) {
-        cl.sync();                                         // every rank's partial dots are final
-        if (crank == 0) {
-          for (int i = threadIdx.x; i < nj; i += kNTs) {
-            uint64_t d = ((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i];
-            for (int r = 1; r < csize; ++r) {
-              const uint32_t* rl = cl.map_shared_rank(sm.dot_lo, r);
-              const uint32_t* rh = cl.map_shared_rank(sm.dot_hi, r);
-              d += ((uint64_t)rh[i] << 32) | rl[i];
-            }
-            sm.dot_lo[i] = (uint32_t)d;
-            sm.dot_hi[i] = (uint32_t)(d >> 32);
-          }
-        }
-        cl.sync();                                         // remote reads done before ranks reuse them
-        if (crank != 0) continue;                          // ranks > 0 only stream (uniform per CTA)
-      }
-      if (jb == 0) DBG_T(11);
-      if (jb == 0 && (a.dbg_skip & 8) && threadIdx.x == 0 && blockIdx.x < 2048)
-        g_dbg_t[blockIdx.x * kDbgSlots + 13] = clock64();
-      for (int i = threadIdx.x; i < nj; i += kNTs) {
-        const int64_t gj = gfirst + jb + i;
-        if (a.step_nbag[gj] == 0) continue;                // void history step (reading R5)
-        const int64_t dot = (int64_t)(((uint64_t)sm.dot_hi[i] << 32) | sm.dot_lo[i]);
-        // sim = <v_curr, v_i> / (||v_curr|| ||v_i||), reading R12
-        const double cs = __ddiv_rn(__ll2double_rn(dot), __dsqrt_rn(__dmul_rn(n2k, __ll2double_rn(a.ws.n2[gj]))));
-        if (cs > a.tau_s) {                                // strict: "exceeding"
-          const int idx = atomicAdd(&sm.count, 1);
-          if (idx < kCandCap) { sm.cs[idx] = cs; sm.js[idx] = (int32_t)(jb + i); }
-          else sm.overflow = 1;
-        }
-      }
-      __syncthreads();
-      if (compact && sm.count > kCandCap / 2) {
-        sort_cands(sm.cs, sm.js, sm.count);
-        __syncthreads();
-        if (threadIdx.x == 0) sm.count = a.top_k;
-        __syncthreads();
-      }
-    }
-    if (crank != 0) continue;
-    DBG_T(2);
-    if (sm.overflow) {
-      if (threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
-      __syncthreads();
-    }
-    int m = sm.count < kCandCap ? sm.count : kCandCap;
-    sort_cands(sm.cs, sm.js, m);
-    if (a.top_k > 0 && m > a.top_k) m = a.top_k;
-    DBG_T(3);
-    // stash the ranked survivors for the fill kernel
-    __shared__ unsigned long long s_base;
-    if (threadIdx.x == 0) {
-      s_base = (m > 0 && !fused) ? atomicAdd(a.ws.stash_alloc, (unsigned long long)m) : 0ull;
-      if (!fused && (int64_t)(s_base + m) > a.match_cap) set_status(a.status, MEMSHARE_ERR_CAPACITY);
-    }
-    __syncthreads();
-    const int64_t base = (int64_t)s_base;
-    for (int r = threadIdx.x; r < m; r += kNTs) {
-      if (!fused && base + r < a.match_cap) { a.ws.stash_cos[base + r] = sm.cs[r]; a.ws.stash_j[base + r] = sm.js[r]; }
-      sm.u.l.jasc[r] = sm.js[r];
-    }
-    if (threadIdx.x == 0) { sm.acc_t = 0u; sm.acc_p = 0u; }
-    __syncthreads();
-    // a4: count targets and deduplicated pairs of this step
-    DBG_T(4);
-    Cands c{m, sm.u.l.jasc, sm.u.l.flo, sm.flen, sm.cum};
-    prepare_cands(a, c, gfirst);
-    DBG_T(5);
-    const int32_t fk_lo = ceil_div(a.step_start[g], a.block_size), fk_hi = a.step_end[g] / a.block_size;
-    const int32_t nt = (m > 0 && fk_hi > fk_lo) ? fk_hi - fk_lo : 0;
-    if (nt > kMaxTgt && threadIdx.x == 0) set_status(a.status, MEMSHARE_ERR_CAPACITY);
-    const int32_t* trow = a.table + (int64_t)s * a.table_stride;
-    int64_t my_t = 0, my_p = 0;
-    // fused fill: the history staging area is free now; it holds the per-target kept counts,
-    // pair offsets and target numbers of the step (kMaxTgt x 16 B = 64 KiB)
-    int32_t* f_tc = reinterpret_cast<int32_t*>(sm.tok);
-    int64_t* f_tpos = reinterpret_cast<int64_t*>(f_tc + kMaxTgt);
-    int32_t* f_tnum = reinterpret_cast<int32_t*>(f_tpos + kMaxTgt);
-    for (int32_t i = w; i < nt && !(a.dbg_skip & 2); i += kNWs) {
-      const int32_t kept = target_sources(a, c, trow, s, i, fk_lo + i, 0, 0, nullptr, 0, 0);
-      my_t += kept > 0 ? 1 : 0;
-      my_p += kept;
-      if (fused && lane == 0 && i < kMaxTgt) f_tc[i] = kept;
-    }
-    if (lane == 0) { atomicAdd(&sm.acc_t, (uint32_t)my_t); atomicAdd(&sm.acc_p, (uint32_t)my_p); }
-    __syncthreads();
-    DBG_T(6);
-    if (threadIdx.x == 0) {
-      a.ws.cnt_m[g] = m;
-      a.ws.cnt_t[g] = (int32_t)sm.acc_t;
-      a.ws.cnt_p[g] = (int32_t)sm.acc_p;
-      a.ws.stash_base[g] = base;
-    }
-    __syncthreads();
-    if (fused) {
-      // offsets of this step's outputs, then the fill kernel's work done here
-      const int4 pre = s1_prefix(a, wi, m, (int32_t)sm.acc_t, (int32_t)sm.acc_p, &s_lb);
-      DBG_T(8);
-      if (wi == nwork - 1) s1_totals(a, make_int4(pre.x + m, pre.y + (int32_t)sm.acc_t, pre.z + (int32_t)sm.acc_p, 0));
-      const int64_t mo = pre.x, to = pre.y, po = pre.z;
-      for (int r = threadIdx.x; r < m; r += kNTs) {
-        if (mo + r < a.match_cap) {
-          memshare_step_match mt;
-          mt.seq = s; mt.step = (int32_t)k; mt.cand_step = sm.js[r]; mt.rank = r; mt.cosine = sm.cs[r];
-          a.matches[mo + r] = mt;
-        }
-      }
-      const int32_t ntf = nt < kMaxTgt ? nt : kMaxTgt;
-      int64_t pcarry = 0, tcarry = 0;
-      for (int32_t ib = 0; ib < ntf; ib += kNTs) {
-        const int32_t i = ib + threadIdx.x;
-        const int64_t v = i < ntf ? f_tc[i] : 0;
-        int64_t tot;
-        const int64_t ex = block_excl_scan<NT>(v, tot, sm.sh);
-        int64_t tt;
-        const int64_t tex = block_excl_scan<NT>(v > 0 ? 1 : 0, tt, sm.sh);
-        if (i < ntf) { f_tpos[i] = pcarry + ex; f_tnum[i] = v > 0 ? (int32_t)(tcarry + tex) : -1; }
-        pcarry += tot;
-        tcarry += tt;
-      }
-      __syncthreads();
-      DBG_T(9);
-      for (int32_t i = w; i < ntf; i += kNWs) {
-        if (f_tnum[i] < 0) continue;
-        const int64_t tidx = to + f_tnum[i];
-        const int32_t tl = fk_lo + i;
-        const int32_t tphys = phys_of(a, trow, tl);
-        target_sources(a, c, trow, s, i, tl, tphys, (int32_t)tidx, a.pairs, po + f_tpos[i], a.pair_cap);
-        if (lane == 0 && tidx < a.target_cap) a.target_off[tidx] = po + f_tpos[i];
-      }
-      __syncthreads();
-    }
+    s1_item<NT>(a, sm, wi, g, s, gfirst, S, fused, nwork, &s_lb);
   }
   DBG_T(7);
   if (!fused && !(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
@@ -1107,6 +1142,7 @@ __global__ void __launch_bounds__(kNT) fill_kernel(CandArgs a) {
     __syncthreads();
   }
 }
+
 
 }  // namespace
 }  // namespace ms

@@ -15,7 +15,7 @@
 //   (q + 1 < n) ? (t[i] in D && t[i+1] not in D) : final[s]          (reading R3).
 #include <climits>
 
-#include "common.cuh"
+#include "segment_impl.cuh"
 
 namespace ms {
 namespace {
@@ -30,34 +30,6 @@ constexpr int kNT = MS_SEG_NT;           // threads per tile
 constexpr int kItems = MS_SEG_ITEMS;     // tokens per thread (a 32-bit flag word each)
 static_assert(kItems <= 32, "per-thread flags are 32-bit masks");
 constexpr int kTile = kNT * kItems;
-
-// (ends, content, bpos, bcb): bpos = position (flat) of the last boundary or -1, bcb = content
-// tokens before bpos counted from the start of the range the aggregate covers.
-struct Agg {
-  int32_t e, c, bpos, bcb;
-};
-
-__device__ __forceinline__ Agg agg_identity() { return Agg{0, 0, -1, 0}; }
-
-// a (earlier range) then b (later range)
-__device__ __forceinline__ Agg combine(const Agg& a, const Agg& b) {
-  Agg r;
-  r.e = a.e + b.e;
-  r.c = a.c + b.c;
-  if (b.bpos >= 0) { r.bpos = b.bpos; r.bcb = a.c + b.bcb; }
-  else { r.bpos = a.bpos; r.bcb = a.bcb; }
-  return r;
-}
-
-__device__ __forceinline__ Agg shfl_agg_up(const Agg& v, int o) {
-  return Agg{__shfl_up_sync(0xffffffffu, v.e, o), __shfl_up_sync(0xffffffffu, v.c, o),
-             __shfl_up_sync(0xffffffffu, v.bpos, o), __shfl_up_sync(0xffffffffu, v.bcb, o)};
-}
-
-__device__ __forceinline__ Agg shfl_agg_down(const Agg& v, int o) {
-  return Agg{__shfl_down_sync(0xffffffffu, v.e, o), __shfl_down_sync(0xffffffffu, v.c, o),
-             __shfl_down_sync(0xffffffffu, v.bpos, o), __shfl_down_sync(0xffffffffu, v.bcb, o)};
-}
 
 struct SegWs {
   int32_t* flag;   // [tiles] 0 = nothing, 1 = aggregate, 2 = inclusive prefix; [tiles] = tile ticket (zeroed per call)

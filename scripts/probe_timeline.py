@@ -49,10 +49,10 @@ def show(title, tl, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--separate", action="store_true", help="a5-a7 as block_distance + remap (default: fused call)")
+    ap.add_argument("--fused", action="store_true", help="a5-a7 as memshare_block_distance_remap")
     args = ap.parse_args()
-    if args.separate:
-        os.environ["MEMSHARE_BENCH_FUSED"] = "0"
+    if args.fused:
+        os.environ["MEMSHARE_BENCH_FUSED"] = "1"
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     ns = argparse.Namespace(collective="nccl", no_graph=False, steps=1, warmup=3)

@@ -36,12 +36,13 @@ def full_parity(w, tau_s=None, tau_b=None, top_k=0, pairing=oracle.ALIGNED, cur_
     tau_s = w.tau_s if tau_s is None else tau_s
     tau_b = w.tau_b if tau_b is None else tau_b
     p.autosize(tau_s, top_k, pairing, cur_mode, cb, ce)
+    p.segment()
+    p.candidates(tau_s, top_k, pairing, cur_mode, cb, ce)
     if fused:
-        p.segment()
-        p.candidates(tau_s, top_k, pairing, cur_mode, cb, ce)
         p.distance_remap(tau_b)
     else:
-        p.round(tau_s, tau_b, top_k, pairing, cur_mode, cb, ce)
+        p.distance_call(tau_b)
+        p.remap()
     torch.cuda.synchronize()
     return check_round(p, w, tau_s, tau_b, top_k, pairing, cur_mode, cb, ce)
 
@@ -472,6 +473,69 @@ def test_segment_edge_cases():
                          delims, out[0], out[1], out[2], sso, 10, ws, status)
     torch.cuda.synchronize()
     assert rc == 0 and status.item() == L.CAPACITY and int(sso[-1]) == n
+
+
+def _edge_trace():
+    """Ragged, empty, one-token, delimiter-only, prompt-only, long multi-delimiter and ragged-tail
+    sequences (test_segment_edge_cases' traces)."""
+    rng = np.random.default_rng(0)
+    seqs = [np.zeros(0, np.int32), np.asarray([5], np.int32), np.asarray([1, 1, 1], np.int32),
+            rng.choice([1, 2, 3, 4, 9], 20000, p=[0.05, 0.02, 0.31, 0.31, 0.31]).astype(np.int32),
+            rng.choice([1, 3, 4], 4097, p=[0.3, 0.35, 0.35]).astype(np.int32),
+            np.asarray([3, 3, 1, 4, 1], np.int32), rng.choice([1, 3, 4, 5, 6], 3000).astype(np.int32)]
+    toks = np.concatenate(seqs)
+    off = np.concatenate([[0], np.cumsum([q.size for q in seqs])]).astype(np.int64)
+    gs = np.asarray([0, 0, 1, 100, 0, 9, 40], np.int32)
+    fin = np.asarray([1, 0, 1, 1, 0, 0, 1], np.uint8)
+    return toks, off, gs, fin, np.asarray([1, 2], np.int32)
+
+
+@pytest.mark.parametrize("tau_s,top_k,pairing,step_cap", [(-1.0, 7, oracle.ALIGNED, None), (0.3, 5, oracle.CROSS, None),
+                                                          (0.5, 0, oracle.ALIGNED, 40)])
+def test_online_round_edge_cases(tau_s, top_k, pairing, step_cap):
+    """An online round (cur_mode LAST: 8-CTA Stage-1 clusters) on the segmentation edge cases --
+    empty, one-token, prompt-only, delimiter-only, non-final, multi-delimiter and 20k-token
+    sequences -- against the oracle's segmentation and Stage 1; with a step capacity below the step
+    count: CAPACITY, the required size in seq_step_off, the steps below the capacity written, and
+    no Stage-1 output for the sequences whose last step is beyond it."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    from paper_2507_21433_b200.pipeline import Caps, MemSharePath
+    toks, off, gs, fin, delims = _edge_trace()
+    S = off.size - 1
+    bs = SMALL.block_size
+    nbl = [-(-(int(off[i + 1] - off[i])) // bs) for i in range(S)]
+    perm = np.random.default_rng(5).permutation(sum(nbl)).astype(np.int32)
+    table = np.zeros((S, max(nbl)), np.int32)
+    o = 0
+    for i in range(S):
+        table[i, :nbl[i]] = perm[o:o + nbl[i]]
+        o += nbl[i]
+    nb = int(sum(nbl))
+    p = MemSharePath(toks, off, gs, fin, delims, table, np.ones(nb, np.int32), np.full(nb, -1, np.int32), 0,
+                     None, None, 0, 0, nb, SMALL.num_layers, SMALL.num_kv_heads, SMALL.num_kv_heads, SMALL.head_dim, bs)
+    if step_cap is not None:
+        p.set_caps(Caps(step=step_cap, match=p.caps.match, pair=p.caps.pair, target=p.caps.target))
+    p.segment()
+    p.candidates(tau_s, top_k, pairing, oracle.CUR_LAST)
+    torch.cuda.synchronize()
+    st, steps, cand = p.read_status(), p.read_steps(), p.read_candidates()
+    exp = oracle.segment_steps(toks, off, gs, fin, delims)
+    if step_cap is None:
+        assert st == 0
+        assert_steps_equal(steps, exp)
+        oc = oracle.step_candidates(toks, off, exp, delims, table, bs, tau_s, top_k, pairing, oracle.CUR_LAST)
+        assert_candidates_equal(cand, oc)
+        assert oc["matches"]["seq"].size > 0
+    else:
+        assert st == L.CAPACITY and steps["seq_step_off"][-1] == exp["seq_step_off"][-1] > step_cap
+        assert np.array_equal(steps["seq_step_off"], exp["seq_step_off"])
+        for k in ("step_start", "step_end", "step_nbag"):
+            assert np.array_equal(steps[k], exp[k][:step_cap]), k
+        # Stage 1 only for the sequences whose last step lies below the capacity
+        below = [q for q in range(S) if exp["seq_step_off"][q + 1] <= step_cap]
+        got_seqs = set(np.unique(cand["matches"]["seq"]).tolist())
+        assert got_seqs <= set(below)
 
 
 def test_long_step_uses_global_table():
