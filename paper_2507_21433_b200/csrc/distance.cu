@@ -92,7 +92,8 @@ struct DistArgs {
   int32_t N, d, h_global;
   int32_t slice_bytes, n_sub;
   int32_t cw, wstride;   // consumer warps of the streaming kernel; partials per (pair, layer, K|V, sub) (4 | wstride)
-  int32_t lpi, n_chunks;
+  int32_t lpi, n_chunks;  // layers per work unit (host default); see unit_lpi for the device choice
+  int32_t lpi_auto;      // 1: small lists (< 2 units of lpi layers per CTA) use 1-layer units
   const memshare_block_pair* pairs;
   const int64_t* target_off;
   const int64_t* num_pairs;
@@ -110,7 +111,6 @@ struct DistArgs {
   int32_t* status;
   DistWs ws;
   int32_t fused;         // FULL mode: targets are finalised inside the streaming kernel (no finalize_kernel)
-  uint32_t fin_need;     // fused: unit completions that finish a target (n_chunks)
   int32_t remap;         // fused a5-a7 call: the last CTA applies the decisions (remap_impl.cuh)
   RemapArgs rm;
 };
@@ -154,6 +154,16 @@ __device__ __forceinline__ int64_t clamp_count(const int64_t* p, int64_t cap) {
   const int64_t v = __ldcg(p);
   return v < 0 ? 0 : (v < cap ? v : cap);
 }
+
+// Layers per (target, layer chunk) work unit: the host's lpi, or 1 when the list is so short that
+// lpi-layer units would leave CTAs idle (fewer than two per CTA: an online round's few targets).
+// Every CTA computes the same value from the device target count.
+__device__ __forceinline__ int32_t unit_lpi(const DistArgs& a) {
+  if (!a.lpi_auto || a.lpi <= 1) return a.lpi;
+  const int64_t T = clamp_count(a.num_targets, a.target_cap);
+  return T * (int64_t)a.n_chunks < 2 * (int64_t)gridDim.x ? 1 : a.lpi;
+}
+__device__ __forceinline__ int32_t unit_chunks(const DistArgs& a, int32_t lpi) { return (a.N + lpi - 1) / lpi; }
 
 // fixed-order fp32 sum of the per-warp partials of (row, layer l, kv) of one workspace buffer
 // (L1 = false: L2 loads, for partials other CTAs wrote; true: plain loads, for partials this CTA's
@@ -301,8 +311,9 @@ __device__ __forceinline__ void unit_terms(const DistArgs& a, int64_t t, int32_t
   int64_t p1 = __ldcg(a.target_off + t + 1);
   if (p1 > P) p1 = P;
   const int N = a.N;
-  const int32_t l0 = lc * a.lpi;
-  const int32_t nl = (l0 + a.lpi < N ? l0 + a.lpi : N) - l0;
+  const int32_t lpi = unit_lpi(a);
+  const int32_t l0 = lc * lpi;
+  const int32_t nl = (l0 + lpi < N ? l0 + lpi : N) - l0;
   const double inv = 1.0 / (2.0 * (double)a.d * (double)a.h_global);
   const int64_t ne = (p1 > p0 ? p1 - p0 : 0) * nl;
   for (int64_t e = lane; e < ne; e += 32) {
@@ -459,7 +470,7 @@ __device__ __forceinline__ void unit_start(const DistArgs& a, FinQ& q, int64_t t
 
 // Count `n` completed units of target t (one lane); true when that completes the target.
 __device__ __forceinline__ bool count_units(const DistArgs& a, int64_t t, uint32_t n) {
-  return atomicAdd(a.ws.tcnt + t, n) + n == a.fin_need;
+  return atomicAdd(a.ws.tcnt + t, n) + n == (uint32_t)unit_chunks(a, unit_lpi(a));
 }
 
 // The finaliser warp.
@@ -561,7 +572,8 @@ __device__ __forceinline__ void st_producer(StSmem<KRE, CW>& sm, const DistArgs&
   constexpr int NS = StCfg<KRE, CW>::kNSt;
   const int64_t I = clamp_count(a.num_targets, a.target_cap);
   const int64_t Pn = clamp_count(a.num_pairs, a.pair_cap);
-  const int64_t total = I * a.n_chunks;
+  const int32_t lpi = unit_lpi(a);
+  const int64_t total = I * unit_chunks(a, lpi);
   int stage = 0;
   uint32_t ph = 0;
   // one unit = (target, chunk of lpi layers); the next unit's ids are loaded one unit ahead
@@ -601,8 +613,8 @@ __device__ __forceinline__ void st_producer(StSmem<KRE, CW>& sm, const DistArgs&
     if (cur.np > 0 && a.fused) unit_start(a, q, cur.t, cur.lc, lane);
     if (cur.np > 0) {
       const int32_t tphys = checked_phys(a, cur.tphys);
-      const int32_t l0 = (int32_t)cur.lc * a.lpi;
-      const int32_t l1 = (l0 + a.lpi < a.N) ? l0 + a.lpi : a.N;
+      const int32_t l0 = (int32_t)cur.lc * lpi;
+      const int32_t l1 = (l0 + lpi < a.N) ? l0 + lpi : a.N;
       for (int32_t c0 = 0; c0 < cur.np; c0 += 64) {
         const int32_t cn = (cur.np - c0) < 64 ? cur.np - c0 : 64;
         int32_t sa = cur.sp0, sb = cur.sp1;
@@ -1029,6 +1041,7 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
     if (lpi_env < 0) lpi_env = 0;
   }
   a.lpi = lpi_env > 0 ? lpi_env : 2;
+  a.lpi_auto = lpi_env > 0 ? 0 : 1;
   if (a.lpi > a.N) a.lpi = a.N;
   a.n_chunks = (a.N + a.lpi - 1) / a.lpi;
   a.pairs = pairs; a.target_off = target_off; a.num_pairs = num_pairs; a.num_targets = num_targets;
@@ -1038,7 +1051,6 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
   a.ws = dist_layout(w, a.N, a.n_sub, a.wstride, pair_cap, target_cap, metric);
   // FULL mode finalises inside the streaming kernel (MEMSHARE_FUSED_TAIL=0: the finalize kernel, A/B)
   a.fused = (mode == MEMSHARE_DIST_FULL && (rm != nullptr || fused_tail_env())) ? 1 : 0;
-  a.fin_need = (uint32_t)a.n_chunks;
   if (rm) {
     a.remap = 1;
     a.rm = *rm;

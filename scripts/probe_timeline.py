@@ -20,7 +20,7 @@ import bench  # noqa: E402
 from paper_2507_21433_b200 import _lib as L  # noqa: E402
 
 NAMES = {0: "flag_reset", 1: "seg", 2: "encode", 3: "stage1", 4: "fill", 5: "ticket_reset", 6: "distance_st",
-         7: "finalize", 8: "remap"}
+         7: "finalize", 8: "remap", 9: "chain_link"}
 TUS = ("segment", "candidates", "distance", "remap")
 
 
@@ -84,6 +84,38 @@ def main():
     g.replay()
     torch.cuda.synchronize()
     show("online LAST round (one graph)", read(True), 1)
+
+    # the busiest online round: each sequence's step with the most Stage-1 survivors (cur_mode RANGE)
+    mt = p.read_candidates()["matches"]
+    r.restore()
+    p.segment()
+    p.candidates(w.tau_s)
+    torch.cuda.synchronize()
+    mt = p.read_candidates()["matches"]
+    busiest = np.zeros(w.batch.num_seqs, np.int32)
+    for sq in range(w.batch.num_seqs):
+        st = mt["step"][mt["seq"] == sq]
+        if st.size:
+            busiest[sq] = np.bincount(st).argmax()
+    bb = torch.as_tensor(busiest, device=dev)
+    be = bb + 1
+
+    def busy():
+        r.restore()
+        p.segment()
+        p.candidates(w.tau_s, cur_mode=L.CUR_RANGE, cur_begin=bb, cur_end=be)
+        r.distance()
+        r.remap_phase()
+    busy()
+    torch.cuda.synchronize()
+    gb = p.capture(busy)
+    for _ in range(5):
+        gb.replay()
+    torch.cuda.synchronize()
+    read(True)
+    gb.replay()
+    torch.cuda.synchronize()
+    show(f"busiest online round (RANGE, {int(p.num_pairs.item())} pairs, one graph)", read(True), 1)
 
 
 if __name__ == "__main__":
