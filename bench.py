@@ -53,14 +53,14 @@ BATCH_CONFIGS = ("c3", "c4", "c5")
 POOL_BUDGET = 140e9          # KV bytes one wave may take on a 180 GB B200 (the rest: workspaces, CUDA)
 
 
-def gpu_launches_per_step(num_tokens, sms=148, fused_tail=True):
-    """Our kernels per round: flag reset, seg, encode, stage1, (fill), counter reset, distance
-    (+ finalize, remap unless a5-a7 is the fused memshare_block_distance_remap call, which
-    finalises and remaps inside the streaming kernel). The library fuses the fill into stage1 for
-    an offline round over at most 100 x 8 x SMs tokens (one CoT-sized batch);
-    MEMSHARE_FUSED_FILL=0 disables it."""
+def gpu_launches_per_step(num_tokens, sms=148, fused_tail=False):
+    """Our kernels per round: flag reset, seg, encode, stage1, (fill), ticket reset, distance,
+    finalize, remap (inside finalize's last CTA when a5-a7 is the fused
+    memshare_block_distance_remap call). The library fuses the fill into stage1 for an offline
+    round over at most 100 x 8 x SMs tokens (one CoT-sized batch); MEMSHARE_FUSED_FILL=0 disables
+    it."""
     fused = num_tokens <= 100 * 8 * sms and os.environ.get("MEMSHARE_FUSED_FILL", "1") != "0"
-    return (6 if fused_tail else 8) + (0 if fused else 1)
+    return (7 if fused_tail else 8) + (0 if fused else 1)
 
 
 def parse():
@@ -393,9 +393,9 @@ class Run:
                 print(f"bench: symmetric memory unavailable ({e!r}); using the NCCL all-reduce", file=sys.stderr)
                 self.collective = "nccl"
         self.world = world
-        # a5-a6 (targets finalised inside the streaming kernel) then a7 as separate calls;
+        # a5-a6 then a7 as separate calls (the roofline times the a5-a6 call alone);
         # MEMSHARE_BENCH_FUSED=1 times memshare_block_distance_remap (a5-a7 in one call: the remap in
-        # the streaming kernel's last CTA) -- measured ~4 us per round slower on B200
+        # the finalisation kernel's last CTA; same offline step, busiest online round -1.5 us)
         self.fused = mode != "headshard" and os.environ.get("MEMSHARE_BENCH_FUSED", "0") == "1"
         torch.cuda.synchronize()
         self.pristine = p.state.clone()
@@ -777,10 +777,10 @@ def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_na
          "pairs_per_s_a5a6": P / (d_ms / 1e3), "kv_bytes": kv_bytes, "distinct_blocks": U, "peak_source": peak_src,
          "frac_of_nominal_8000": achieved / 8000.0,
          "note": ("achieved/kernel_ms: CUDA events around the whole a5-a7 call (memshare_block_distance_remap: "
-                  "counter reset + streaming kernel with the finalisation and the remap fused in; conservative: the "
+                  "ticket reset + streaming kernel + finalize with the remap in its last CTA; conservative: the "
                   "remap is inside)" if "remap" in kernel_name else
-                  "achieved/kernel_ms: CUDA events around the whole a5-a6 call (counter reset + streaming kernel, "
-                  "the targets finalised inside it; conservative)") +
+                  "achieved/kernel_ms: CUDA events around the whole a5-a6 call (ticket reset + streaming kernel "
+                  "+ finalize, conservative)") +
                  " over K steps replayed phase by phase right after the timed loop (which replays each step as one "
                  "graph); kernel_only_*: events around the streaming kernel alone (library profiling hook, eager "
                  "calls)"}

@@ -261,10 +261,9 @@ size_t memshare_remap_workspace_size(int32_t num_blocks, int64_t target_cap);
  * validation failure changes nothing). Arguments are those of the two calls; num_blocks is
  * pool_host->num_blocks; partial_sq is not produced.
  *   workspace >= memshare_block_distance_remap_workspace_size() bytes.
- * Implementation: every target is finalised inside the streaming kernel by the consumer warp that
- * completes its last (target, layer chunk) unit (per-target completion counts), and the last CTA of
- * the streaming kernel to finish applies the decisions -- two launches (counter reset, stream)
- * instead of four. Errors: as memshare_block_distance and memshare_remap. */
+ * Implementation: the streaming kernel and the finalisation kernel of memshare_block_distance; the
+ * finalisation kernel's last CTA to finish then applies the decisions -- one launch fewer than the
+ * two calls. Errors: as memshare_block_distance and memshare_remap. */
 memshare_status memshare_block_distance_remap(
     const memshare_kv_pool* pool_host, const memshare_dims* dims_host, const memshare_block_pair* pairs,
     const int64_t* target_off, const int64_t* num_pairs, const int64_t* num_targets, int64_t pair_cap,

@@ -20,7 +20,8 @@
 //     FFMA2 (fp32), a warp-shuffle sum, one fp32 partial per warp (fixed order, no fp atomics).
 //  finalize_kernel -- one CTA per target: fixed-order fp32 sums of the warp partials, fp64 sqrt,
 //   /(2dh), layer mean, fp32 distance, the strict tau_b test and the argmin with the
-//   smaller-source-logical tie break.
+//   smaller-source-logical tie break; for memshare_block_distance_remap its last CTA then applies
+//   the decisions (remap_impl.cuh).
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
@@ -41,28 +42,21 @@ constexpr int kFinWarps = kFinThreads / 32;
 constexpr int kPhi4Slice = 40960;
 constexpr int kRingBytes = 224 * 1024;                      // shared-memory ring (of 227 KB per CTA)
 constexpr int kMaxKre = 10;                                 // largest stage: 40 KiB (one Phi-4 slice)
-constexpr int kMaxCw = 10;                                  // consumer warps of the largest instantiation
 constexpr int kMaxRingStages = 48;
 #ifndef MS_ST_MAXKRE
 #define MS_ST_MAXKRE kMaxKre      // tuning: cap on the stage size, in 4 KiB units
 #endif
 
-// stage codes; H_END marks the last stage of a (target, layer chunk) unit
-constexpr int H_STOP = 1, H_ANCHOR = 2, H_PAIR = 4, H_END = 8;
+constexpr int H_STOP = 1, H_ANCHOR = 2, H_PAIR = 4;
 
-// a stage header (one 16-byte shared load for the consumers):
-//   {out lo, out hi, bytes | code << 24, target}     (bytes <= 40 KiB)
-__device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t code, int32_t target = 0) {
-  return make_int4((int32_t)(uint32_t)(uint64_t)out, (int32_t)((uint64_t)out >> 32), bytes | (code << 24), target);
+// a stage header (one 16-byte shared load for the consumers): {out lo, out hi, bytes, code}
+__device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t code) {
+  return make_int4((int32_t)(uint32_t)(uint64_t)out, (int32_t)((uint64_t)out >> 32), bytes, code);
 }
-__device__ __forceinline__ int hcode(int4 h) { return (int)((uint32_t)h.z >> 24); }
-__device__ __forceinline__ int32_t hbytes(int4 h) { return h.z & 0xFFFFFF; }
 
 struct DistWs {
   unsigned int* ticket;
-  unsigned int* cta_done;  // fused tail: CTAs past their stream (the last one runs the remap)
-  unsigned int* tcnt;    // fused tail: [target_cap] completed (target, layer chunk) units per target
-  double* terms;         // fused tail: [pair_cap][N] per-(pair, layer) terms of Alg. 1 line 5
+  unsigned int* fin_done;  // finalize CTAs done (memshare_block_distance_remap: the last one remaps)
   float* wpart;          // [pair_cap][N][2][n_sub][wstride]  per consumer warp: squared sums of t - s (both metrics)
   float* wsn;            // cosine only: [pair_cap][N][2][n_sub][W] source squared norms
   float* wtn;            // cosine only: [target_cap][N][2][n_sub][W] target squared norms
@@ -72,9 +66,7 @@ DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t wstride, int64_t pai
                    int32_t metric) {
   DistWs d;
   d.ticket = w.take<unsigned int>(2);
-  d.cta_done = d.ticket ? d.ticket + 1 : nullptr;
-  d.tcnt = w.take<unsigned int>((size_t)target_cap + 1);
-  d.terms = w.take<double>((size_t)pair_cap * N + 1);
+  d.fin_done = d.ticket ? d.ticket + 1 : nullptr;
   const size_t per = (size_t)N * 2 * n_sub * wstride;
   d.wpart = w.take<float>((size_t)pair_cap * per + 1);
   const bool cosine = metric == MEMSHARE_METRIC_COSINE;
@@ -93,7 +85,7 @@ struct DistArgs {
   int32_t slice_bytes, n_sub;
   int32_t cw, wstride;   // consumer warps of the streaming kernel; partials per (pair, layer, K|V, sub) (4 | wstride)
   int32_t lpi, n_chunks;  // layers per work unit (host default); see unit_lpi for the device choice
-  int32_t lpi_auto;      // 1: small lists (< 2 units of lpi layers per CTA) use 1-layer units
+  int32_t lpi_auto;      // 1: short lists (< 2 units of lpi layers per CTA) take 1-layer units
   const memshare_block_pair* pairs;
   const int64_t* target_off;
   const int64_t* num_pairs;
@@ -110,8 +102,7 @@ struct DistArgs {
   memshare_decision* decisions;
   int32_t* status;
   DistWs ws;
-  int32_t fused;         // FULL mode: targets are finalised inside the streaming kernel (no finalize_kernel)
-  int32_t remap;         // fused a5-a7 call: the last CTA applies the decisions (remap_impl.cuh)
+  int32_t remap;         // memshare_block_distance_remap: the finalize kernel's last CTA remaps
   RemapArgs rm;
 };
 
@@ -163,19 +154,15 @@ __device__ __forceinline__ int32_t unit_lpi(const DistArgs& a) {
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
   return T * (int64_t)a.n_chunks < 2 * (int64_t)gridDim.x ? 1 : a.lpi;
 }
-__device__ __forceinline__ int32_t unit_chunks(const DistArgs& a, int32_t lpi) { return (a.N + lpi - 1) / lpi; }
 
 // fixed-order fp32 sum of the per-warp partials of (row, layer l, kv) of one workspace buffer
-// (L1 = false: L2 loads, for partials other CTAs wrote; true: plain loads, for partials this CTA's
-// warps wrote -- the fused tail's finaliser)
-template <bool L1 = false>
 __device__ __forceinline__ float sum_warps(const DistArgs& a, const float* buf, int64_t row, int32_t l, int32_t kv) {
   const int q4 = a.wstride / 4;
   const float4* w = reinterpret_cast<const float4*>(buf + (((row * a.N + l) * 2 + kv) * a.n_sub) * a.wstride);
   float s = 0.f;
   for (int sub = 0; sub < a.n_sub; ++sub) {
     for (int j = 0; j < q4; ++j) {                       // warps 0 .. cw-1 in order (the padding is skipped)
-      const float4 v = L1 ? w[sub * q4 + j] : __ldcg(w + sub * q4 + j);
+      const float4 v = __ldcg(w + sub * q4 + j);
       const int c = a.cw - 4 * j;
       s = s + v.x;
       if (c > 1) s = s + v.y;
@@ -295,241 +282,6 @@ __device__ void finalize_target(const DistArgs& a, int64_t t, double* terms, int
   }
 }
 
-// The finaliser reads the partials its CTA's consumer warps stored, ordered by a CTA-scope fence:
-// plain (L1-path) loads. Measured on B200: L2-only loads (__ldcg) after the same CTA-scope fence
-// could return stale partials (the f2 cosine parity test caught it); a gpu-scope fence in every
-// consumer warp at every unit end instead cost the streaming kernel ~10 %.
-constexpr bool kFtL1 = true;
-
-// Fused tail, per completed (target t, layer chunk lc) unit: the per-(pair, layer) terms of
-// Alg. 1 line 5 (Euclidean: (sqrt(sum_K) + sqrt(sum_V)) / 2dh; cosine: mean of the two 1 - cos),
-// from the consumer warps' partials in the same fixed order as finalize_target, into ws.terms
-// (lanes over the unit's (pair, layer) entries). Run by the finaliser warp while the stream goes on.
-__device__ __forceinline__ void unit_terms(const DistArgs& a, int64_t t, int32_t lc, int lane) {
-  const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
-  const int64_t p0 = __ldcg(a.target_off + t);
-  int64_t p1 = __ldcg(a.target_off + t + 1);
-  if (p1 > P) p1 = P;
-  const int N = a.N;
-  const int32_t lpi = unit_lpi(a);
-  const int32_t l0 = lc * lpi;
-  const int32_t nl = (l0 + lpi < N ? l0 + lpi : N) - l0;
-  const double inv = 1.0 / (2.0 * (double)a.d * (double)a.h_global);
-  const int64_t ne = (p1 > p0 ? p1 - p0 : 0) * nl;
-  for (int64_t e = lane; e < ne; e += 32) {
-    const int64_t p = p0 + e / nl;
-    const int32_t l = l0 + (int32_t)(e % nl);
-    double term;
-    if (a.metric == MEMSHARE_METRIC_COSINE) {
-      const double ck = one_minus_cos(sum_warps<kFtL1>(a, a.ws.wpart, p, l, 0), sum_warps<kFtL1>(a, a.ws.wtn, t, l, 0),
-                                      sum_warps<kFtL1>(a, a.ws.wsn, p, l, 0));
-      const double cv = one_minus_cos(sum_warps<kFtL1>(a, a.ws.wpart, p, l, 1), sum_warps<kFtL1>(a, a.ws.wtn, t, l, 1),
-                                      sum_warps<kFtL1>(a, a.ws.wsn, p, l, 1));
-      term = 0.5 * (ck + cv);
-    } else {
-      const float sk = sum_warps<kFtL1>(a, a.ws.wpart, p, l, 0);
-      const float sv = sum_warps<kFtL1>(a, a.ws.wpart, p, l, 1);
-      if (a.partial_sq != nullptr) {
-        a.partial_sq[(p * N + l) * 2 + 0] = sk;
-        a.partial_sq[(p * N + l) * 2 + 1] = sv;
-      }
-      term = (__dsqrt_rn((double)sk) + __dsqrt_rn((double)sv)) * inv;
-    }
-    a.ws.terms[p * N + l] = term;
-  }
-}
-
-// Fused tail: ONE warp finalises target t once all its units' terms are in ws.terms: the layer
-// mean in finalize_target's order (lane l accumulates the terms l, l+32, ... then one butterfly),
-// so distances and decisions are bit-identical to the finalize_kernel path; the argmin runs on the
-// values in registers.
-__device__ __forceinline__ void warp_finalize(const DistArgs& a, int64_t t, int lane) {
-  const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
-  const int64_t p0 = __ldcg(a.target_off + t);
-  int64_t p1 = __ldcg(a.target_off + t + 1);
-  if (p1 > P) p1 = P;
-  const int N = a.N;
-  int64_t b = -1;
-  float bd = 0.f;
-  int32_t bl = 0;
-  auto take = [&](int64_t p, double acc, int32_t lp) {
-    acc = warp_sum(acc);
-    const float D = (float)(acc / (double)N);                           // Alg. 1 line 7
-    if (lane == 0) {
-      a.distance[p] = D;
-      a.under[p] = D < a.tau_b ? 1 : 0;
-    }
-    if (b < 0 || D < bd || (D == bd && lp < bl)) { b = p; bd = D; bl = lp; }
-  };
-  if (N <= 64) {
-    // pairs four at a time: every lane issues its term loads (and one source_logical) of the four
-    // pairs before any sum, so a target costs one memory latency per four pairs
-    constexpr int kG = 4;
-    for (int64_t g0 = p0; g0 < p1; g0 += kG) {
-      double v0[kG], v1[kG];
-#pragma unroll
-      for (int q = 0; q < kG; ++q) {
-        const bool in = g0 + q < p1;
-        v0[q] = (in && lane < N) ? __ldcg(a.ws.terms + (g0 + q) * N + lane) : 0.0;
-        v1[q] = (in && lane + 32 < N) ? __ldcg(a.ws.terms + (g0 + q) * N + lane + 32) : 0.0;
-      }
-      const int32_t my_lp = (lane < kG && g0 + lane < p1) ? __ldg(&a.pairs[g0 + lane].source_logical) : 0;
-#pragma unroll
-      for (int q = 0; q < kG; ++q) {
-        double acc = 0.0;                                 // l = lane, lane + 32 in order
-        if (lane < N) acc += v0[q];
-        if (lane + 32 < N) acc += v1[q];
-        const int32_t lp = __shfl_sync(0xffffffffu, my_lp, q);
-        if (g0 + q < p1) take(g0 + q, acc, lp);
-      }
-    }
-  } else {
-    for (int64_t p = p0; p < p1; ++p) {
-      double acc = 0.0;
-      for (int l = lane; l < N; l += 32) acc += __ldcg(a.ws.terms + p * N + l);
-      take(p, acc, a.pairs[p].source_logical);
-    }
-  }
-  if (lane == 0) {
-    memshare_decision dc;
-    dc.num_candidates = (int32_t)(p1 > p0 ? p1 - p0 : 0);
-    if (b < 0) {
-      dc.seq = -1; dc.target_logical = -1; dc.target_phys = -1; dc.source_logical = -1; dc.source_phys = -1;
-      dc.accepted = 0; dc.distance = INFINITY;
-    } else {
-      const memshare_block_pair pr = a.pairs[b];
-      dc.seq = pr.seq; dc.target_logical = pr.target_logical; dc.target_phys = pr.target_phys;
-      dc.source_logical = pr.source_logical; dc.source_phys = pr.source_phys;
-      dc.distance = bd;
-      dc.accepted = bd < a.tau_b ? 1 : 0;              // strict (reading R21)
-    }
-    if (t < a.target_cap) a.decisions[t] = dc;
-    __threadfence();                                   // before this CTA's completion count (fused remap)
-  }
-}
-
-#ifdef MS_FT_PROF
-// tuning only: per-CTA timestamps of the fused tail [cta][0 start, 1 producer done, 2 consumers done,
-// 3 finaliser done, 4 finalisations, 5 batches, 6 first finalisation, 7 time in warp_finalize]
-__device__ unsigned long long g_ft_prof[1024][8];
-__device__ __forceinline__ unsigned long long ft_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define FT_PROF(i, v) do { if (lane == 0 && blockIdx.x < 1024) g_ft_prof[blockIdx.x][i] = (v); } while (0)
-#else
-#define FT_PROF(i, v) do { } while (0)
-#endif
-
-// Fused tail bookkeeping of a CTA. The producer records the target of every unit it starts
-// (unit_t ring); each consumer warp counts the unit-end stages it has evaluated (wdone, after a
-// CTA-scope fence over its partial stores); the finaliser warp takes the units every consumer warp
-// has finished, in order, and -- one gpu-scope fence per batch -- adds them to the targets'
-// global unit counts; the unit that completes a target (n_chunks units) makes it finalise the
-// target. Nothing on the consumers' path waits for a gpu-scope fence (one per unit cost the
-// streaming kernel ~25 % at c2).
-constexpr int kUnitQ = 128;
-struct FinQ {
-  int32_t unit_t[kUnitQ];
-  int32_t unit_lc[kUnitQ];
-  unsigned int wdone[kMaxCw];    // per consumer warp: unit-end stages evaluated
-  unsigned int started;          // units the producer has started (and recorded)
-  unsigned int counted;          // units the finaliser has counted (frees their unit_t slots)
-  unsigned int prod_done;        // the producer is past its last unit
-};
-
-__device__ __forceinline__ unsigned int ld_vol(const unsigned int* p) { return *reinterpret_cast<const volatile unsigned int*>(p); }
-__device__ __forceinline__ void st_vol(unsigned int* p, unsigned int v) { *reinterpret_cast<volatile unsigned int*>(p) = v; }
-
-// consumer warp, after evaluating (and releasing) a unit-end stage
-__device__ __forceinline__ void unit_end(FinQ& q, int warp, int lane, unsigned int& my_units) {
-  __syncwarp();
-  ++my_units;
-  if (lane == 0) {
-    __threadfence_block();                             // this warp's partial stores before the count
-    st_vol(&q.wdone[warp], my_units);
-  }
-}
-
-// producer, before the first stage of a unit with stages
-__device__ __forceinline__ void unit_start(const DistArgs& a, FinQ& q, int64_t t, int64_t lc, int lane) {
-  if (lane == 0) {
-    const unsigned int k = q.started;
-    SpinGuard sg;
-    while (k - ld_vol(&q.counted) >= (unsigned)kUnitQ) {   // ring full: the finaliser is behind
-      if (sg.expired()) { set_status(a.status, MEMSHARE_ERR_CORRUPTION); break; }
-    }
-    q.unit_t[k % kUnitQ] = (int32_t)t;
-    q.unit_lc[k % kUnitQ] = (int32_t)lc;
-    __threadfence_block();
-    st_vol(&q.started, k + 1);
-  }
-  __syncwarp();
-}
-
-// Count `n` completed units of target t (one lane); true when that completes the target.
-__device__ __forceinline__ bool count_units(const DistArgs& a, int64_t t, uint32_t n) {
-  return atomicAdd(a.ws.tcnt + t, n) + n == (uint32_t)unit_chunks(a, unit_lpi(a));
-}
-
-// The finaliser warp.
-__device__ __forceinline__ void finaliser_loop(const DistArgs& a, FinQ& q, int lane, int cw) {
-  unsigned int k = 0;                                  // units counted
-#ifdef MS_FT_PROF
-  unsigned long long nfin = 0, nbatch = 0, tfin = 0;
-#endif
-  for (;;) {
-    const unsigned int pd = ld_vol(&q.prod_done);      // read before the counts below
-    unsigned int avail = lane < cw ? ld_vol(&q.wdone[lane]) : 0xFFFFFFFFu;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned int y = __shfl_xor_sync(0xffffffffu, avail, o);
-      avail = y < avail ? y : avail;
-    }
-    if (avail > k) {
-#ifdef MS_FT_PROF
-      ++nbatch;
-#endif
-      __threadfence_block();                           // the consumers' partial stores (CTA scope) before reading them
-      for (unsigned int j = k; j < avail; ++j) unit_terms(a, q.unit_t[j % kUnitQ], q.unit_lc[j % kUnitQ], lane);
-      __threadfence();                                 // the batch's terms before the counts
-      for (unsigned int j0 = k; j0 < avail; j0 += 32) {
-        const unsigned int j = j0 + lane;
-        int32_t t = -1;
-        if (j < avail) {
-          t = q.unit_t[j % kUnitQ];
-          if (!count_units(a, t, 1u)) t = -1;
-        }
-        unsigned int fin = __ballot_sync(0xffffffffu, t >= 0);
-        while (fin) {                                  // targets this batch completed, in unit order
-          const int src = __ffs(fin) - 1;
-          fin &= fin - 1;
-          const int32_t tt = __shfl_sync(0xffffffffu, t, src);
-          __threadfence();
-#ifdef MS_FT_PROF
-          const unsigned long long f0 = ft_now();
-          if (nfin == 0) FT_PROF(6, f0);
-#endif
-          warp_finalize(a, (int64_t)tt, lane);
-#ifdef MS_FT_PROF
-          ++nfin;
-          tfin += ft_now() - f0;
-#endif
-        }
-      }
-      k = avail;
-      if (lane == 0) st_vol(&q.counted, k);
-      continue;
-    }
-    if (pd != 0u && k == ld_vol(&q.started)) break;    // the producer is done and every unit is counted
-    __nanosleep(128);
-  }
-  FT_PROF(3, ft_now());
-  FT_PROF(4, nfin);
-  FT_PROF(5, nbatch);
-  FT_PROF(7, tfin);
-}
 
 __device__ __forceinline__ int32_t checked_phys(const DistArgs& a, int32_t p) {
   if (p < 0 || p >= a.num_blocks) {
@@ -563,17 +315,15 @@ struct StSmem {
   alignas(16) int4 hdr[StCfg<KRE, CW>::kNSt];
   alignas(8) uint64_t full[StCfg<KRE, CW>::kNSt];
   uint64_t empty[StCfg<KRE, CW>::kNSt];
-  FinQ fq;
 };
 
 template <int KRE, int CW>
 __device__ __forceinline__ void st_producer(StSmem<KRE, CW>& sm, const DistArgs& a, int lane) {
-  FinQ& q = sm.fq;
   constexpr int NS = StCfg<KRE, CW>::kNSt;
   const int64_t I = clamp_count(a.num_targets, a.target_cap);
   const int64_t Pn = clamp_count(a.num_pairs, a.pair_cap);
   const int32_t lpi = unit_lpi(a);
-  const int64_t total = I * unit_chunks(a, lpi);
+  const int64_t total = I * ((a.N + lpi - 1) / lpi);
   int stage = 0;
   uint32_t ph = 0;
   // one unit = (target, chunk of lpi layers); the next unit's ids are loaded one unit ahead
@@ -605,12 +355,6 @@ __device__ __forceinline__ void st_producer(StSmem<KRE, CW>& sm, const DistArgs&
     int64_t next2 = 0;
     if (lane == 0) next2 = (int64_t)atomicAdd(a.ws.ticket, 1u);
     const UnitMeta nm = load_meta(next);
-    if (cur.np <= 0 && a.fused) {                      // a unit without stages (clamped pairs): count it here
-      bool fin = false;
-      if (lane == 0) { __threadfence(); fin = count_units(a, cur.t, 1u); }
-      if (__shfl_sync(0xffffffffu, fin, 0)) { __threadfence(); warp_finalize(a, cur.t, lane); }
-    }
-    if (cur.np > 0 && a.fused) unit_start(a, q, cur.t, cur.lc, lane);
     if (cur.np > 0) {
       const int32_t tphys = checked_phys(a, cur.tphys);
       const int32_t l0 = (int32_t)cur.lc * lpi;
@@ -636,11 +380,9 @@ __device__ __forceinline__ void st_producer(StSmem<KRE, CW>& sm, const DistArgs&
                   // output row: the pair (Euclidean / cosine dot) or, for the target stage, the
                   // target (cosine: its squared norm)
                   const int64_t po = q < 0 ? cur.t : (int64_t)(cur.lo + c0 + q);
-                  const bool end = q == cn - 1 && sub == a.n_sub - 1 && kv == 1 && l == l1 - 1 &&
-                                   c0 + 64 >= cur.np;              // the unit's last stage
                   mbar_wait(&sm.empty[stage], ph ^ 1u);
                   sm.hdr[stage] = make_hdr((((po * a.N + l) * 2 + kv) * a.n_sub + sub) * a.wstride, bytes,
-                                           (q < 0 ? H_ANCHOR : H_PAIR) | (end ? H_END : 0), (int32_t)cur.t);
+                                           q < 0 ? H_ANCHOR : H_PAIR);
                   mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
                   bulk_g2s(sm.ring[stage], base + (int64_t)phys * a.block_stride_b + boff, (uint32_t)bytes,
                            &sm.full[stage]);
@@ -672,7 +414,7 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
     // f2 (reading R34): target stage -> cache + squared norm; source stage -> |t - s|^2 + squared norm
     const int64_t o = (int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp;
     float2 n0 = make_float2(0.f, 0.f), n1 = n0;
-    if (hcode(h) & H_ANCHOR) {
+    if (h.w & H_ANCHOR) {
 #pragma unroll
       for (int r = 0; r < KRE; ++r) {
         const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
@@ -682,7 +424,7 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
       }
       const float tn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
       if (lane == 0) a.ws.wtn[o] = tn;
-    } else if (hcode(h) & H_PAIR) {
+    } else if (h.w & H_PAIR) {
       // squared difference (the same accumulator as the Euclidean metric) and the source norm
       float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
@@ -701,7 +443,7 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
     }
     return;
   }
-  if (hcode(h) & H_ANCHOR) {
+  if (h.w & H_ANCHOR) {
 #pragma unroll
     for (int r = 0; r < KRE; ++r) {
       T[4 * r + 0] = bf2_to_f2(x[r].x);
@@ -709,7 +451,7 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
       T[4 * r + 2] = bf2_to_f2(x[r].z);
       T[4 * r + 3] = bf2_to_f2(x[r].w);
     }
-  } else if (hcode(h) & H_PAIR) {
+  } else if (h.w & H_PAIR) {
     float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int r = 0; r < KRE; ++r) {
@@ -735,7 +477,7 @@ __device__ __forceinline__ void st_eval_probe(const DistArgs& a, int4 h, const u
   uint32_t f = 0u;
 #pragma unroll
   for (int r = 0; r < KRE; ++r) f ^= x[r].x ^ x[r].y ^ x[r].z ^ x[r].w;
-  if (f == 0x9E3779B9u && (hcode(h) & H_PAIR)) a.ws.wpart[(int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp] = 1.f;
+  if (f == 0x9E3779B9u && (h.w & H_PAIR)) a.ws.wpart[(int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x) + warp] = 1.f;
 }
 #define ST_EVAL(h, x) st_eval_probe<KRE, MET>(a, h, x, warp, lane)
 #else
@@ -743,7 +485,7 @@ __device__ __forceinline__ void st_eval_probe(const DistArgs& a, int4 h, const u
 #endif
 
 template <int KRE, int CW, int MET, bool PARTIAL>
-__global__ void __launch_bounds__(CW * 32 + 64, 1) distance_st_kernel(DistArgs a) {
+__global__ void __launch_bounds__(CW * 32 + 32, 1) distance_st_kernel(DistArgs a) {
   constexpr int NS = StCfg<KRE, CW>::kNSt;
   constexpr int NC = CW * 32;                            // consumer threads
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -756,114 +498,73 @@ __global__ void __launch_bounds__(CW * 32 + 64, 1) distance_st_kernel(DistArgs a
       mbar_init(&sm.empty[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    sm.fq.started = 0u;
-    sm.fq.counted = 0u;
-    sm.fq.prod_done = 0u;
   }
-  if (tid < kMaxCw) sm.fq.wdone[tid] = 0u;
   __syncthreads();
   pdl_trigger();
   TL_SCOPE(6);
-  if (warp == CW + 1) {
-    // fused tail: the finaliser warp (idle when the finalize kernel runs instead)
-    FT_PROF(0, ft_now());
-    if (a.fused) finaliser_loop(a, sm.fq, lane, CW);
-  } else if (warp == CW) {
+  if (warp == CW) {
     st_producer<KRE, CW>(sm, a, lane);
-    if (lane == 0) { __threadfence_block(); st_vol(&sm.fq.prod_done, 1u); }
-    FT_PROF(1, ft_now());
-  } else {
-    // consumers: ping-pong register buffers (the next stage is copied while this one is evaluated)
-    float2 T[KRE * 4];
-    uint4 xa[KRE], xb[KRE];
-    int stage = 0;
-    uint32_t ph = 0;
-    unsigned int my_units = 0;                           // fused tail: unit-end stages evaluated
-    // a stage is full except possibly the last sub-slice of a slice that is not a multiple of the
-    // stage: its missing chunks are zero on both sides (target and source), adding nothing
-    auto load = [&](uint4 (&dst)[KRE], int32_t bytes) {
-      const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
-      if (!PARTIAL || bytes == StCfg<KRE, CW>::kStageB) {   // exact geometries: no predicates at all
+    return;
+  }
+  // consumers: ping-pong register buffers (the next stage is copied while this one is evaluated)
+  float2 T[KRE * 4];
+  uint4 xa[KRE], xb[KRE];
+  int stage = 0;
+  uint32_t ph = 0;
+  // a stage is full except possibly the last sub-slice of a slice that is not a multiple of the
+  // stage: its missing chunks are zero on both sides (target and source), adding nothing
+  auto load = [&](uint4 (&dst)[KRE], int32_t bytes) {
+    const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
+    if (!PARTIAL || bytes == StCfg<KRE, CW>::kStageB) {   // exact geometries: no predicates at all
 #pragma unroll
-        for (int r = 0; r < KRE; ++r) dst[r] = src[tid + r * NC];
-      } else {
-        const int nchunk = bytes >> 4;
+      for (int r = 0; r < KRE; ++r) dst[r] = src[tid + r * NC];
+    } else {
+      const int nchunk = bytes >> 4;
 #pragma unroll
-        for (int r = 0; r < KRE; ++r) {
-          const int c = tid + r * NC;
-          dst[r] = c < nchunk ? src[c] : make_uint4(0u, 0u, 0u, 0u);
-        }
+      for (int r = 0; r < KRE; ++r) {
+        const int c = tid + r * NC;
+        dst[r] = c < nchunk ? src[c] : make_uint4(0u, 0u, 0u, 0u);
       }
-    };
-    auto release = [&]() {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[stage]);
-      if (++stage == NS) { stage = 0; ph ^= 1u; }
-    };
-    // fused tail: after the last stage of a unit (and after releasing the stage this warp holds)
-    auto after = [&](int4 h) {
-      if (a.fused && (hcode(h) & H_END)) unit_end(sm.fq, warp, lane, my_units);
-    };
+    }
+  };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (++stage == NS) { stage = 0; ph ^= 1u; }
+  };
+  mbar_wait(&sm.full[stage], ph);
+  int4 ha = sm.hdr[stage], hb;
+  if (ha.w & H_STOP) return;
+  load(xa, ha.z);
+  release();
+  for (;;) {
     mbar_wait(&sm.full[stage], ph);
-    int4 ha = sm.hdr[stage], hb;
-    if (!(hcode(ha) & H_STOP)) {
-      load(xa, hbytes(ha));
-      release();
-      for (;;) {
-        mbar_wait(&sm.full[stage], ph);
-        hb = sm.hdr[stage];
-        if (!(hcode(hb) & H_STOP)) load(xb, hbytes(hb));
-        ST_EVAL(ha, xa);
-        if (hcode(hb) & H_STOP) { after(ha); break; }
-        release();
-        after(ha);
-        mbar_wait(&sm.full[stage], ph);
-        ha = sm.hdr[stage];
-        if (!(hcode(ha) & H_STOP)) load(xa, hbytes(ha));
-        ST_EVAL(hb, xb);
-        if (hcode(ha) & H_STOP) { after(hb); break; }
-        release();
-        after(hb);
-      }
-    }
-    if (warp == 0) FT_PROF(2, ft_now());
-  }
-  if (a.remap) {
-    // fused a7: every target was finalised by a warp of a CTA that has passed this point, so the
-    // last CTA here sees all decisions (each finaliser fenced its decision before its CTA counted)
-    __shared__ int64_t rsh[(CW * 32 + 64) / 32 + 1];
-    __shared__ int rbad;
-    __shared__ bool rlast;
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      rlast = atomicAdd(a.ws.cta_done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (rlast) {
-      __threadfence();
-      remap_cta<CW * 32 + 64>(a.rm, rsh, &rbad);
-    }
+    hb = sm.hdr[stage];
+    if (!(hb.w & H_STOP)) load(xb, hb.z);
+    ST_EVAL(ha, xa);
+    if (hb.w & H_STOP) break;
+    release();
+    mbar_wait(&sm.full[stage], ph);
+    ha = sm.hdr[stage];
+    if (!(ha.w & H_STOP)) load(xa, ha.z);
+    ST_EVAL(hb, xb);
+    if (ha.w & H_STOP) break;
+    release();
   }
 }
 
-// Zeroes the work ticket (and, for the fused tail, the CTA count and the per-target unit counts).
-// A kernel rather than a memset node so the launch chain keeps its programmatic dependent
-// launches (the streaming kernel's CTAs wait for this grid to complete before they take tickets).
-__global__ void ticket_reset_kernel(DistWs ws, const int64_t* num_targets, int64_t target_cap, int fused) {
-  pdl_trigger();
-  TL_SCOPE(5);
-  if (blockIdx.x == 0 && threadIdx.x < 2) ws.ticket[threadIdx.x] = 0u;
-  if (!fused) return;
-  const int64_t T = clamp_count(num_targets, target_cap);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x)
-    ws.tcnt[i] = 0u;
-}
-
-// Finalisation: one CTA per target (grid-stride). PARTIAL (and FULL with
-// MEMSHARE_FUSED_TAIL=0) read the per-warp partials the
+// Finalisation: one CTA per target (grid-stride). FULL/PARTIAL read the per-warp partials the
 // streaming kernel left in the workspace (kernel boundary = the only synchronisation needed);
 // FINALIZE reads partial squared sums already reduced across ranks.
+// Zeroes the work ticket. A kernel rather than a memset node so the launch chain keeps its
+// programmatic dependent launches (the streaming kernel's CTAs wait for this grid to complete
+// before they take tickets).
+__global__ void ticket_reset_kernel(unsigned int* ticket) {
+  pdl_trigger();
+  TL_SCOPE(5);
+  if (threadIdx.x < 2) ticket[threadIdx.x] = 0u;          // the unit ticket and the finalize CTA count
+}
+
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(DistArgs a, int from_partial) {
   pdl_trigger();
   TL_SCOPE(7);
@@ -871,6 +572,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(DistArgs a, int f
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
   for (int64_t t = blockIdx.x; t < T; t += gridDim.x)
     finalize_target(a, t, terms, threadIdx.x, from_partial != 0, [] { __syncthreads(); });
+  if (a.remap && last_block_done(a.ws.fin_done)) {
+    // a7 fused: every decision is written (each CTA's writes precede its count, last_block_done)
+    __shared__ int64_t rsh[kFinThreads / 32 + 1];
+    __shared__ int rbad;
+    remap_cta<kFinThreads>(a.rm, rsh, &rbad);
+  }
 }
 
 // host: stage geometry for a slice -- KRE (16-byte chunks per consumer thread; stage = KRE x 4 KiB)
@@ -912,7 +619,7 @@ static cudaError_t launch_st(const DistArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_pdl(distance_st_kernel<KRE, CW, MET, PARTIAL>, dim3(sm_count()), dim3(CW * 32 + 64),
+  return launch_pdl(distance_st_kernel<KRE, CW, MET, PARTIAL>, dim3(sm_count()), dim3(CW * 32 + 32),
                     sizeof(StSmem<KRE, CW>), st, a);
 }
 
@@ -953,19 +660,7 @@ using namespace ms;
 
 TL_EXPORT(distance)
 
-static bool fused_tail_env() {      // MEMSHARE_FUSED_TAIL=0: separate finalize kernel (A/B)
-  static int on = -1;
-  if (on < 0) { const char* e = getenv("MEMSHARE_FUSED_TAIL"); on = (e && e[0] == '0') ? 0 : 1; }
-  return on == 1;
-}
-
 static thread_local cudaEvent_t g_prof_begin = nullptr, g_prof_end = nullptr;
-
-#ifdef MS_FT_PROF
-extern "C" int memshare_debug_ft_prof(unsigned long long* host) {
-  return (int)cudaMemcpyFromSymbol(host, g_ft_prof, sizeof(g_ft_prof));
-}
-#endif
 
 extern "C" void memshare_profile_distance_events(void* begin, void* end) {
   g_prof_begin = static_cast<cudaEvent_t>(begin);
@@ -1049,8 +744,6 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
   a.distance = distance; a.under = under; a.decisions = decisions; a.status = device_status;
   Ws w{static_cast<char*>(workspace), 0};
   a.ws = dist_layout(w, a.N, a.n_sub, a.wstride, pair_cap, target_cap, metric);
-  // FULL mode finalises inside the streaming kernel (MEMSHARE_FUSED_TAIL=0: the finalize kernel, A/B)
-  a.fused = (mode == MEMSHARE_DIST_FULL && (rm != nullptr || fused_tail_env())) ? 1 : 0;
   if (rm) {
     a.remap = 1;
     a.rm = *rm;
@@ -1065,16 +758,14 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
     launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 1);
     return launch_status();
   }
-  const int64_t rg = (tc + 4095) / 4096;
-  launch_pdl(ticket_reset_kernel, dim3(a.fused ? (unsigned)(rg < 64 ? rg : 64) : 1u), dim3(a.fused ? 1024 : 32), 0, st,
-             a.ws, a.num_targets, a.target_cap, a.fused);
+  launch_pdl(ticket_reset_kernel, dim3(1), dim3(32), 0, st, a.ws.ticket);
   const bool prof = g_prof_begin != nullptr && g_prof_end != nullptr;
   if (prof && cudaEventRecord(g_prof_begin, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   const bool partial = slice_bytes % ((int64_t)kre * 16 * 32 * a.cw) != 0;
   const cudaError_t le = launch_st_any(kre, partial, metric, a, st);
   if (le != cudaSuccess) return MEMSHARE_ERR_CUDA;
   if (prof && cudaEventRecord(g_prof_end, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
-  if (!a.fused) launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 0);
+  launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 0);
   return launch_status();
 }
 

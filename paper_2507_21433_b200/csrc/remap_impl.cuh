@@ -1,6 +1,6 @@
 // a7 zero-copy remap as a CTA-wide device routine, shared by remap_kernel (remap.cu, one
-// 1024-thread CTA) and the fused a5-a7 call (distance.cu: the last CTA of the streaming kernel to
-// finish runs it, memshare_block_distance_remap).
+// 1024-thread CTA) and the fused a5-a7 call (distance.cu: the last CTA of the finalisation kernel
+// to finish runs it, memshare_block_distance_remap).
 // PAPER.md:276-278 ("simply updates the block table"), :283-284 (no extra GPU bandwidth);
 // SPEC.md:358-366; readings R23, R26.
 //

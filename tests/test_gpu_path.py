@@ -269,8 +269,8 @@ def _round_outputs(p):
 
 @pytest.mark.parametrize("case", ["tiny0", "tiny5", "chain", "small", "cross", "phi4", "geom", "two_rounds"])
 def test_fused_distance_remap_matches_separate_calls(case):
-    """memshare_block_distance_remap (a5-a7 in one call: targets finalised inside the streaming
-    kernel by a finaliser warp, the remap run by the streaming kernel's last CTA) against
+    """memshare_block_distance_remap (a5-a7 in one call: the remap run by the finalisation kernel's
+    last CTA) against
     memshare_block_distance + memshare_remap on the same round: distances, under flags, decisions,
     table, refcounts, free list and counters bit-identical, and the fused round passes the full
     oracle check."""
