@@ -713,6 +713,7 @@ class Run:
                 assert out["max_rel_err"] <= 1e-5, "distance rel err"
                 sub_off = np.concatenate([[0], np.cumsum([toff[t + 1] - toff[t] for t in tsel])])
                 best, acc, _ = oracle.select(D, sub_off, pr["source_logical"][psel], w.tau_b)
+                exact = near_tie = near_thr = 0
                 for j, t in enumerate(tsel):
                     p0, p1 = sub_off[j], sub_off[j + 1]
                     src = gd["decisions"]["source_logical"][t]
@@ -720,8 +721,16 @@ class Run:
                     assert m.size == 1, "decision source"
                     dmin = D[p0:p1].min()
                     assert D[p0 + m[0]] <= dmin * (1 + 1e-5), "decision outside the tie set"
-                    if bool(gd["decisions"]["accepted"][t]) != bool(acc[j]):
+                    same_src = p0 + m[0] == best[j]
+                    same_acc = bool(gd["decisions"]["accepted"][t]) == bool(acc[j])
+                    if not same_acc:
                         assert abs(D[best[j]] - np.float32(w.tau_b)) <= 1e-4 * w.tau_b, "accept away from tau_b"
+                    exact += int(same_src and same_acc)
+                    near_tie += int(not same_src)
+                    near_thr += int(not same_acc)
+                # SURVEY.md §5 parity counts (reading R29): decisions equal to the oracle's, and those
+                # allowed to differ (a near tie / a distance within 1e-4 of tau_b)
+                out["decisions"] = {"exact": exact, "near_tie": near_tie, "near_threshold": near_thr}
             s = p.read_state()
             st_o, tab, rc, fl, fc, nf, af = oracle.remap(w.table, w.refcount, w.free_list, w.free_count,
                                                          gd["decisions"], sh.block_size)
@@ -769,7 +778,27 @@ def reduce_max_sum(dist, dev, mx, sm):
     return float(a[0]), float(b[0])
 
 
-def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_name):
+def live_copy_gbs(dev):
+    """This box's copy bandwidth, measured the way MEASURED_PEAKS.json's hbm_gbs is (torch copy of
+    1 Gi bf16 elements, read + write bytes, best of 10, CUDA events): context for box-to-box spread
+    of the roofline fraction (the fraction itself uses the driver-measured peak)."""
+    import torch
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 2 * (1 << 30) / (best / 1e3) / 1e9
+
+
+def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_name, live=None):
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / (d_ms / 1e3) / 1e9
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -787,6 +816,9 @@ def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_na
     if kernel_only_ms:
         r["kernel_only_ms"] = kernel_only_ms
         r["kernel_only_frac"] = alg_bytes / (kernel_only_ms / 1e3) / 1e9 / peak
+    if live:
+        r["live_copy_gbs"] = live
+        r["frac_of_live_copy"] = achieved / live
     return r
 
 
@@ -872,7 +904,7 @@ def run_single(args, rank, world, local):
         "roofline": roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P,
                              committed_traffic(args.config, f"{args.config}_seed{args.seed}"),
                              "distance_st_kernel (memshare_block_distance_remap)" if r.fused
-                             else "distance_st_kernel (memshare_block_distance)"),
+                             else "distance_st_kernel (memshare_block_distance)", live=live_copy_gbs(dev)),
         "per_step": {"pairs": P, "targets": T, "steps": r.counts["steps"], "matches": r.counts["matches"],
                      "freed_blocks": step_freed, "affected_tokens": step_affected},
         "gpu_launches": gpu_launches_per_step(w.num_tokens, torch.cuda.get_device_properties(dev).multi_processor_count,
@@ -1056,7 +1088,7 @@ def run_batch(args, rank, world, local):
         "roofline": roofline(tot["alg"], tot["d_ms"], tot["k_ms"], tot["kv"], tot["U"], tot["pairs"],
                              committed_traffic(cfg, f"{cfg}_{n}seq_{world}gpu_seed{args.seed}"),
                              "distance_st_kernel (memshare_block_distance_remap)" if fused_tail
-                             else "distance_st_kernel (memshare_block_distance)"),
+                             else "distance_st_kernel (memshare_block_distance)", live=live_copy_gbs(dev)),
         "per_step": {"pairs": int(pairs_all), "pairs_rank0": tot["pairs"], "targets_rank0": tot["targets"],
                      "steps_rank0": tot["steps"], "matches_rank0": tot["matches"], "freed_blocks_rank0": tot["freed"],
                      "affected_tokens_rank0": tot["affected"]},

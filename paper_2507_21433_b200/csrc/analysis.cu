@@ -127,6 +127,7 @@ using namespace ms;
 extern "C" memshare_status memshare_similarity_ratio(const memshare_step_match* matches, const int64_t* num_matches,
                                                      int64_t match_cap, int32_t num_seqs, int64_t* redundant_steps,
                                                      int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_similarity_ratio");
   if (!num_matches || !redundant_steps || !device_status || num_seqs < 0 || match_cap < 0 ||
       (match_cap > 0 && !matches))
     return MEMSHARE_ERR_INVALID_ARGUMENT;
@@ -153,6 +154,7 @@ extern "C" memshare_status memshare_all_pairs(const int64_t* seq_tok_off, int32_
                                               int64_t pair_cap, int64_t* num_pairs, int64_t* target_off,
                                               int64_t target_cap, int64_t* num_targets, void* workspace,
                                               size_t workspace_bytes, int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_all_pairs");
   if (!seq_tok_off || !num_pairs || !target_off || !num_targets || !workspace || !device_status || num_seqs < 0 ||
       block_size < 1 || table_stride < 0 || num_blocks < 0 || pair_cap < 0 || target_cap < 0)
     return MEMSHARE_ERR_INVALID_ARGUMENT;

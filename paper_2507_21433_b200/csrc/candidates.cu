@@ -1185,6 +1185,7 @@ extern "C" memshare_status memshare_step_candidates(
     int64_t* num_matches, memshare_block_pair* pairs, int64_t pair_cap, int64_t* num_pairs, int64_t* target_off,
     int64_t target_cap, int64_t* num_targets, void* workspace, size_t workspace_bytes, int32_t* device_status,
     void* stream) {
+  MS_NVTX("memshare_step_candidates");
   if (num_tokens < 0 || num_seqs < 0 || step_cap < 0 || match_cap < 0 || pair_cap < 0 || target_cap < 0)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (num_delims < 1 || num_delims > MEMSHARE_MAX_DELIMS || !delim_ids_host) return MEMSHARE_ERR_INVALID_ARGUMENT;

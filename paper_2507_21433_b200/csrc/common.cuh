@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <utility>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost a pointer test unless a tool is attached
 
 #include "memshare.h"
 
@@ -234,6 +235,14 @@ inline int sm_count() {
   }
   return cached[dev];
 }
+
+// Tracing: every ABI call is an NVTX range named after it (host side: the
+// enqueue, and the call's place in an Nsight Systems timeline / a CUDA-graph capture).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define MS_NVTX(name) ::ms::NvtxRange ms_nvtx_range_(name)
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

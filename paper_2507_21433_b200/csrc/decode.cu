@@ -478,6 +478,7 @@ extern "C" memshare_status memshare_kv_append(void* k_pool, void* v_pool, int64_
                                               int32_t* free_list, int64_t* free_count, const void* new_k,
                                               const void* new_v, void* workspace, size_t workspace_bytes,
                                               int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_kv_append");
   if (!dims_host || num_seqs < 0 || num_blocks < 0 || table_stride < 0 || !workspace || !device_status)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   const memshare_dims d = *dims_host;
@@ -524,6 +525,7 @@ extern "C" memshare_status memshare_paged_attention_decode(
     int32_t num_q_heads, const int32_t* block_table, int32_t table_stride, const int32_t* seq_len, int32_t num_seqs,
     int32_t max_seq_len, float scale, float* out, void* workspace, size_t workspace_bytes, int32_t* device_status,
     void* stream) {
+  MS_NVTX("memshare_paged_attention_decode");
   if (!pool_host || !dims_host || !workspace || !device_status || num_seqs < 0 || max_seq_len < 0)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   const memshare_dims d = *dims_host;

@@ -776,6 +776,7 @@ extern "C" memshare_status memshare_block_distance(const memshare_kv_pool* pool,
                                                    int32_t metric, float* partial_sq, float tau_b, float* distance,
                                                    uint8_t* under, memshare_decision* decisions, void* workspace,
                                                    size_t workspace_bytes, int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_block_distance");
   return block_distance_impl(pool, dims, pairs, target_off, num_pairs, num_targets, pair_cap, target_cap, mode, metric,
                              partial_sq, tau_b, distance, under, decisions, workspace, workspace_bytes, device_status,
                              stream, nullptr);
@@ -794,6 +795,7 @@ extern "C" memshare_status memshare_block_distance_remap(
     int32_t* block_table, int32_t table_stride, int32_t num_seqs, int32_t* refcount, int32_t* free_list,
     int64_t* free_count, int32_t block_size, int64_t* num_freed, int64_t* affected_tokens, void* workspace,
     size_t workspace_bytes, int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_block_distance_remap");
   if (!pool || !remap_args_ok(block_table, table_stride, num_seqs, refcount, pool->num_blocks, free_list, free_count,
                               num_freed, affected_tokens, block_size))
     return MEMSHARE_ERR_INVALID_ARGUMENT;
@@ -809,6 +811,7 @@ extern "C" memshare_status memshare_block_distance_finalize_peers(
     const memshare_block_pair* pairs, const int64_t* target_off, const int64_t* num_pairs,
     const int64_t* num_targets, int64_t pair_cap, int64_t target_cap, float tau_b, float* distance, uint8_t* under,
     memshare_decision* decisions, void* workspace, size_t workspace_bytes, int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_block_distance_finalize_peers");
   if (!partial_peers || num_peers < 1 || num_peers > 64 || !dims || !pairs || !target_off || !num_pairs ||
       !num_targets || !distance || !under || !decisions || !workspace || !device_status)
     return MEMSHARE_ERR_INVALID_ARGUMENT;

@@ -39,6 +39,7 @@ extern "C" memshare_status memshare_remap(int32_t* block_table, int32_t table_st
                                           const int64_t* num_targets, int64_t target_cap, int32_t block_size,
                                           int64_t* num_freed, int64_t* affected_tokens, void* workspace,
                                           size_t workspace_bytes, int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_remap");
   if (!decisions || !num_targets || !workspace || !device_status || target_cap < 0 ||
       !remap_args_ok(block_table, table_stride, num_seqs, refcount, num_blocks, free_list, free_count, num_freed,
                      affected_tokens, block_size))

@@ -326,6 +326,7 @@ extern "C" memshare_status memshare_segment_steps(const int32_t* tokens, int64_t
                                                   int32_t* step_start, int32_t* step_end, int32_t* step_nbag,
                                                   int64_t* seq_step_off, int64_t step_cap, void* workspace,
                                                   size_t workspace_bytes, int32_t* device_status, void* stream) {
+  MS_NVTX("memshare_segment_steps");
   if (num_tokens < 0 || num_tokens > (int64_t)INT32_MAX - kTile || num_seqs < 0 || step_cap < 0 || num_delims < 1 ||
       num_delims > MEMSHARE_MAX_DELIMS)
     return MEMSHARE_ERR_INVALID_ARGUMENT;

@@ -232,6 +232,43 @@ class MemSharePath:
         self.distance_call(tau_b)
         self.remap()
 
+    # ------------------------------------------------------------------ state snapshot (debugging)
+    def snapshot(self) -> dict:
+        """JSON-serialisable state of the path (SURVEY.md §5 / SPEC.md:412: capacity, dims, tables,
+        refcounts, fill): the KV geometry and caps, the block table, refcounts, the live part of the
+        free list, the round counters and the device status. Synchronises."""
+        st = self.read_state()
+        c = self.counts()
+        d = self.dims
+        fc = st["free_count"]
+        return {"version": 1, "num_seqs": self.num_seqs, "num_tokens": self.num_tokens,
+                "num_blocks": self.num_blocks, "table_stride": self.table_stride,
+                "dims": {"num_layers": d.num_layers, "num_kv_heads_local": d.num_kv_heads_local,
+                         "num_kv_heads_global": d.num_kv_heads_global, "head_dim": d.head_dim,
+                         "block_size": d.block_size},
+                "caps": {"step": self.caps.step, "match": self.caps.match, "pair": self.caps.pair,
+                         "target": self.caps.target},
+                "table": st["table"].tolist(), "refcount": st["refcount"].tolist(),
+                "free_list": st["free_list"][:max(0, min(fc, st["free_list"].size))].tolist(), "free_count": fc,
+                "counters": {**c, "freed": st["num_freed"], "affected_tokens": st["affected"]},
+                "status": self.read_status()}
+
+    def restore_snapshot(self, snap: dict):
+        """Write a snapshot's block table, refcounts, free list and free count back to the device
+        (same geometry; the KV pool and the trace are not part of a snapshot)."""
+        if snap.get("version") != 1 or snap["num_blocks"] != self.num_blocks or \
+                snap["table_stride"] != self.table_stride or snap["num_seqs"] != self.num_seqs:
+            raise ValueError("snapshot does not match this path's geometry")
+        tab = torch.as_tensor(np.asarray(snap["table"], np.int32).reshape(-1), device=self.dev)
+        rc = torch.as_tensor(np.asarray(snap["refcount"], np.int32), device=self.dev)
+        fl = np.full(self.free_list.numel(), -1, np.int32)
+        fl[:len(snap["free_list"])] = np.asarray(snap["free_list"], np.int32)
+        self.table.view(-1).copy_(tab)
+        self.refcount.copy_(rc)
+        self.free_list.copy_(torch.as_tensor(fl, device=self.dev))
+        self.free_count.fill_(int(snap["free_count"]))
+        torch.cuda.synchronize(self.dev)
+
     # ------------------------------------------------------------------ host reads (sync)
     def read_status(self) -> int:
         return int(self.status.item())

@@ -742,6 +742,89 @@ def test_device_errors():
     assert p2.read_status() == L.CORRUPTION
 
 
+def test_state_snapshot_round_trip():
+    """SURVEY.md §5 JSON state snapshot: the path state after a round survives a JSON
+    round trip; restored into a fresh path on the pristine trace, the next round gives the same
+    decisions and state as the original path's next round; the T0 round's snapshot holds the
+    golden free list and affected tokens (tests/golden/tiny_t0.json)."""
+    import json
+    import os
+    import torch
+    w = workloads.small(SMALL, 2, 2500, seed=11, eta=0.0)
+    p = make_path(w)
+    p.autosize(0.5)
+    p.round(0.5, 1e-3)
+    snap = json.loads(json.dumps(p.snapshot()))
+    assert snap["status"] == 0 and snap["counters"]["freed"] > 0
+    assert len(snap["free_list"]) == snap["free_count"]
+    q = make_path(w, caps=p.caps)
+    q.restore_snapshot(snap)
+    for path in (p, q):
+        path.round(0.5, 1e-3)
+    torch.cuda.synchronize()
+    a, b = p.read_distance(), q.read_distance()
+    for k in a["decisions"]:
+        assert np.array_equal(a["decisions"][k], b["decisions"][k]), k
+    sa, sb = p.read_state(), q.read_state()
+    for k in ("table", "refcount", "free_list", "free_count", "num_freed", "affected"):
+        assert np.array_equal(sa[k], sb[k]), k
+    # golden T0
+    t0 = workloads.tiny(eta=0.0)
+    pt = make_path(t0)
+    pt.autosize(t0.tau_s)
+    pt.round(t0.tau_s, t0.tau_b)
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tiny_t0.json")))
+    st = pt.snapshot()
+    assert st["free_list"] == g["free_list"] and st["counters"]["affected_tokens"] == g["affected_tokens"]
+    with pytest.raises(ValueError):
+        make_path(w, caps=p.caps).restore_snapshot(st)       # another geometry
+
+
+def test_fault_injection_refcount_and_free_list():
+    """SURVEY.md §5 fault injection (SPEC.md:607 'corrupted bound'): a refcount corrupted to drive
+    a block below zero, and a free list without room for the freed blocks, are reported as
+    CORRUPTION by the remap (and a corrupted source id in the pair list by the distance call)."""
+    import torch
+    from paper_2507_21433_b200 import _lib as L
+    w = workloads.small(SMALL, 2, 2500, seed=11, eta=0.0)
+    # (1) a refcount of 0 on a block the remap decrements: final count -1
+    p = make_path(w)
+    p.autosize(0.5)
+    p.segment()
+    p.candidates(0.5)
+    p.distance_call(1e-3)
+    torch.cuda.synchronize()
+    dec = p.read_distance()["decisions"]
+    acc = np.nonzero(dec["accepted"])[0]
+    tab = p.table.view(p.num_seqs, p.table_stride).cpu().numpy()
+    olds = [int(tab[dec["seq"][i], dec["target_logical"][i]]) for i in acc]
+    srcs = set(dec["source_phys"][acc].tolist())
+    cand = [o for o, i in zip(olds, acc) if o not in srcs and o != dec["source_phys"][i]]
+    assert cand, "no accepted decision whose old block is nobody's source"
+    p.refcount[cand[0]] = 0
+    p.remap()
+    torch.cuda.synchronize()
+    assert p.read_status() == L.CORRUPTION
+    # (2) the free list already full: no room for the freed blocks
+    p2 = make_path(w)
+    p2.autosize(0.5)
+    p2.free_count.fill_(w.num_blocks)
+    p2.round(0.5, 1e-3)
+    torch.cuda.synchronize()
+    assert p2.read_status() == L.CORRUPTION
+    # (3) a source physical id out of range in the pair list
+    p3 = make_path(w)
+    p3.autosize(0.5)
+    p3.segment()
+    p3.candidates(0.5)
+    torch.cuda.synchronize()
+    pr = p3.pairs.view(torch.int32).view(-1, 6)
+    pr[0, 5] = w.num_blocks + 3
+    p3.distance_call(1e-3)
+    torch.cuda.synchronize()
+    assert p3.read_status() == L.CORRUPTION
+
+
 def test_generator_twins_bit_identical():
     w = workloads.small(SMALL, 2, 1500, seed=3)
     p = make_path(w)
