@@ -62,9 +62,10 @@ struct CandWs {
   int2* gtab;            // [4*num_tokens] {key, count} global tables of oversize steps
   int4* lb_agg;          // [step_cap] fused fill: {matches+1, targets+1, pairs+1, 1} of the step, 0 = not yet
                          // published (zeroed by encode)
+  int64_t* cur_off;      // [num_seqs+1] RANGE work items: exclusive prefix of the current-step counts (encode)
 };
 
-CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_cap) {
+CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_cap, int32_t num_seqs) {
   CandWs c;
   c.done = w.take<unsigned int>(1);
   c.stash_alloc = w.take<unsigned long long>(1);
@@ -82,6 +83,7 @@ CandWs cand_layout(Ws& w, int64_t num_tokens, int64_t step_cap, int64_t match_ca
   c.stash_j = w.take<int32_t>(match_cap + 1);
   c.gtab = w.take<int2>(4 * num_tokens + 1);
   c.lb_agg = w.take<int4>(step_cap + 1);
+  c.cur_off = w.take<int64_t>((size_t)(num_seqs > 0 ? num_seqs : 0) + 1);
   return c;
 }
 
@@ -116,6 +118,7 @@ struct CandArgs {
   int64_t* num_targets;
   int32_t* status;
   int32_t fused;        // offline single-CoT launch: stage1 writes matches / pairs itself (no fill kernel)
+  int32_t range_items;  // RANGE with the fused fill: work items are the current steps only (a dense list)
   int32_t dbg_skip;     // tuning only (env MEMSHARE_DEBUG_SKIP): bit3 phase stamps; in -DMEMSHARE_TUNING builds also
                         // bit0 skip history stream, bit1 pair count, bit2 last-CTA scan, bit4 table probes
   CandWs ws;
@@ -209,6 +212,52 @@ __device__ __forceinline__ int32_t seq_of_step(const CandArgs& a, int64_t g) {
   return lo;
 }
 
+// RANGE: the current local steps [b, e) of sequence s, clamped to its steps below the capacity
+__device__ __forceinline__ void cur_range(const CandArgs& a, int32_t s, int64_t G, int64_t& b, int64_t& e) {
+  const int64_t g0 = a.seq_step_off[s];
+  int64_t g1 = a.seq_step_off[s + 1];
+  if (g1 > G) g1 = G;
+  const int64_t S = g1 > g0 ? g1 - g0 : 0;
+  b = a.cur_begin[s];
+  e = a.cur_end[s];
+  b = b < 0 ? 0 : (b > S ? S : b);
+  e = e < b ? b : (e > S ? S : e);
+}
+
+// RANGE work items (range_items): one block of the encode kernel writes cur_off, the exclusive
+// prefix over the sequences of their current-step counts (all NT threads of that block)
+template <int NT>
+__device__ void range_item_offsets(const CandArgs& a, int64_t G, int64_t* sh) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < a.num_seqs; base += NT) {
+    const int64_t s = base + threadIdx.x;
+    int64_t n = 0;
+    if (s < a.num_seqs) {
+      int64_t b, e;
+      cur_range(a, (int32_t)s, G, b, e);
+      n = e - b;
+    }
+    int64_t tot;
+    const int64_t ex = block_excl_scan<NT>(n, tot, sh);
+    if (s < a.num_seqs) a.ws.cur_off[s] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) a.ws.cur_off[a.num_seqs] = carry;
+}
+
+// RANGE work item i -> its step g (global)
+__device__ __forceinline__ int64_t range_item_step(const CandArgs& a, int64_t i, int64_t G, int32_t& s_out) {
+  int32_t lo = 0, hi = a.num_seqs - 1;                  // last s with cur_off[s] <= i
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (__ldcg(a.ws.cur_off + mid) <= i) lo = mid; else hi = mid - 1;
+  }
+  int64_t b, e;
+  cur_range(a, lo, G, b, e);
+  s_out = lo;
+  return a.seq_step_off[lo] + b + (i - __ldcg(a.ws.cur_off + lo));
+}
+
 // publication keys of the fused fill: steps (offline) or sequences (online LAST rounds)
 __device__ __forceinline__ int64_t fill_keys(const CandArgs& a, int64_t G) {
   const int64_t z = a.cur_mode == MEMSHARE_CUR_LAST ? (int64_t)a.num_seqs : G;
@@ -230,6 +279,7 @@ __global__ void __launch_bounds__(kNT) encode_kernel(CandArgs a) {
     *a.ws.stash_alloc = 0ull;
     *a.ws.ticket = 0ull;
   }
+  if (a.range_items && blockIdx.x == gridDim.x - 1) range_item_offsets<kNT>(a, G, sh);
   for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
     const int32_t s = seq_of_step(a, g);
     const int64_t tok_base = a.seq_tok_off[s];
@@ -313,6 +363,10 @@ __global__ void __launch_bounds__(kNT) encode_warp_kernel(CandArgs a) {
     *a.ws.done = 0u;
     *a.ws.stash_alloc = 0ull;
     *a.ws.ticket = 0ull;
+  }
+  if (a.range_items && blockIdx.x == gridDim.x - 1) {
+    __shared__ int64_t sh[kNW + 1];
+    range_item_offsets<kNT>(a, G, sh);
   }
   for (int64_t g = (int64_t)blockIdx.x * kNW + w; g < G; g += (int64_t)gridDim.x * kNW) {
     const int32_t s = seq_of_step(a, g);
@@ -763,6 +817,15 @@ __device__ void s1_publish_nothing(const CandArgs& a, int64_t key, int64_t nwork
   }
 }
 
+// Publish "no outputs" for the keys [k0, k1) (all CTA threads; the last key also the totals).
+template <int NT>
+__device__ void s1_publish_zero_range(const CandArgs& a, int64_t k0, int64_t k1, int64_t nwork,
+                                                   int4* s_lb) {
+  for (int64_t key = k0 + threadIdx.x; key < k1; key += NT)
+    if (key != nwork - 1) s1_st_relaxed(a.ws.lb_agg + key, make_int4(1, 1, 1, 1));
+  if (k0 <= nwork - 1 && nwork - 1 < k1) s1_publish_nothing<NT>(a, nwork - 1, nwork, s_lb);
+}
+
 // One Stage-1 work item: current step g (local k) of sequence s (steps [gfirst, gfirst + S)):
 // table, history stream (this CTA's share of a cluster's), selection, pair counts and -- fused --
 // the fill. All threads of the CTA (and of its cluster) call it.
@@ -969,7 +1032,9 @@ __device__ void s1_item(const CandArgs& a, SelSmem<NT>& sm, int64_t wi, int64_t 
   }
 }
 
-template <int NT>
+// RI: the RANGE-work-item instantiation (a separate kernel keeps the ALL / LAST kernels' code --
+// run once per launch, instruction-fetch sensitive -- as small as before)
+template <int NT, bool RI = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   constexpr int kNTs = NT, kNWs = NT / 32;
   static_assert(NT != 1024 || kMaxTgt * 16 <= S1Cfg<1024>::kTok * 4, "fused fill reuses the staging area");
@@ -992,10 +1057,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   // the counts of every other step are zeroed up front by all threads (one parallel pass instead
   // of a chain of dependent loads per skipped step) for the last-CTA scan.
   const bool last_mode = a.cur_mode == MEMSHARE_CUR_LAST;
+  const bool range_items = RI && fused && a.range_items != 0;
+  // publication keys: sequences (LAST) or steps; work items: the keys, or -- RANGE with the fused
+  // fill -- the current steps only, each publishing zeros for the non-current keys before it (the
+  // last one also for those after it)
   const int64_t nwork = last_mode ? a.num_seqs : G;
+  const int64_t nitems = range_items ? __ldcg(a.ws.cur_off + a.num_seqs) : nwork;
   // fused fill: work item wi publishes its counts at key wi (= g offline, = the sequence online);
   // the last key also writes the totals
-  if (fused && nwork == 0 && blockIdx.x == 0) s1_totals(a, make_int4(0, 0, 0, 0));
+  if (fused && (nwork == 0 || nitems == 0) && blockIdx.x == 0) s1_totals(a, make_int4(0, 0, 0, 0));
+  auto publish_zero_range = [&](int64_t k0, int64_t k1) { s1_publish_zero_range<NT>(a, k0, k1, nwork, &s_lb); };
   auto publish_nothing = [&](int64_t key) {     // a work item without outputs (all CTA threads call it)
     if (key == nwork - 1) {
       const int4 pre = s1_prefix(a, key, 0, 0, 0, &s_lb);
@@ -1028,20 +1099,34 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
       cl.sync();
       wi = (int64_t)*cl.map_shared_rank(&s_ticket, 0);
     }
-    if (wi >= nwork) {
+    if (wi >= nitems) {
       // rank 0 may not exit while another rank still reads its s_ticket over DSMEM
       if (csize > 1) cl.sync();
       break;
     }
-    const int64_t g = last_mode ? a.seq_step_off[wi + 1] - 1 : wi;
-    if (last_mode && (g < a.seq_step_off[wi] || g >= G)) {            // sequence without steps
-      if (fused && crank == 0) publish_nothing(wi);
-      continue;
+    // one s1_item call site (a second inlined copy costs instruction-cache misses: this code runs
+    // once per launch)
+    int64_t key, g;
+    int32_t s;
+    if (range_items) {
+      g = range_item_step(a, wi, G, s);
+      int32_t sp;
+      const int64_t gprev = wi > 0 ? range_item_step(a, wi - 1, G, sp) : -1;
+      if (crank == 0) publish_zero_range(gprev + 1, g);          // the non-current keys before g
+      key = g;
+    } else {
+      g = last_mode ? a.seq_step_off[wi + 1] - 1 : wi;
+      if (last_mode && (g < a.seq_step_off[wi] || g >= G)) {            // sequence without steps
+        if (fused && crank == 0) publish_nothing(wi);
+        continue;
+      }
+      s = a.ws.step_seq[g];
+      key = wi;
     }
-    const int32_t s = a.ws.step_seq[g];
     const int64_t gfirst = a.seq_step_off[s];
     const int64_t S = a.seq_step_off[s + 1] - gfirst;
-    s1_item<NT>(a, sm, wi, g, s, gfirst, S, fused, nwork, &s_lb);
+    s1_item<NT>(a, sm, key, g, s, gfirst, S, fused, nwork, &s_lb);
+    if (range_items && wi == nitems - 1 && crank == 0) publish_zero_range(g + 1, nwork);   // and after the last
   }
   DBG_T(7);
   if (!fused && !(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
@@ -1166,7 +1251,7 @@ extern "C" size_t memshare_step_candidates_workspace_size(int64_t num_tokens, in
                                                           int64_t match_cap) {
   if (num_tokens < 0 || num_seqs < 0 || step_cap < 0 || match_cap < 0) return 0;
   Ws w{nullptr, 0};
-  cand_layout(w, num_tokens, step_cap, match_cap);
+  cand_layout(w, num_tokens, step_cap, match_cap, num_seqs);
   return w.size();
 }
 
@@ -1228,13 +1313,15 @@ extern "C" memshare_status memshare_step_candidates(
     a.dbg_skip = dbg;
   }
   Ws w{static_cast<char*>(workspace), 0};
-  a.ws = cand_layout(w, num_tokens, step_cap, match_cap);
+  a.ws = cand_layout(w, num_tokens, step_cap, match_cap, num_seqs);
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   static bool attr_set_dev[kMaxDevices] = {};
   bool& attr_set = attr_set_dev[current_device()];
   if (!attr_set) {
     cudaFuncSetAttribute(stage1_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem<1024>));
+    cudaFuncSetAttribute(stage1_kernel<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SelSmem<1024>));
     cudaFuncSetAttribute(stage1_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SelSmem<512>));
     cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemSlots * sizeof(int2)));
     cudaFuncSetAttribute(encode_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1250,26 +1337,33 @@ extern "C" memshare_status memshare_step_candidates(
   const int64_t enc_ctas = enc_warp ? (gcap + kNW - 1) / kNW : gcap;
   const int grid_enc = (int)(enc_ctas < 8 * sms ? enc_ctas : 8 * sms);
   const int grid_sel = (int)(gcap < 2 * sms ? gcap : 2 * sms);
+  // Stage-1 shape (decided first: the encode kernel prepares RANGE work items for it). Cluster
+  // size per current step: online rounds (LAST: one current step per sequence; RANGE: work items
+  // are the current steps, sized for a few per sequence) split each step's history over up to 8
+  // CTAs while the clusters still fit in one wave; offline (ALL) keeps one CTA per step.
+  // MEMSHARE_S1_CLUSTER overrides the online size (tuning / regression tests).
+  static int env_cs = -1;
+  if (env_cs < 0) { const char* e = getenv("MEMSHARE_S1_CLUSTER"); env_cs = e ? atoi(e) : 0; }
+  int cs = 1;
+  if (env_cs > 0 && cur_mode != MEMSHARE_CUR_ALL) cs = env_cs;    // forced (tuning / regression tests)
+  else if (cur_mode != MEMSHARE_CUR_ALL)
+    for (int c = 8; c > 1; c >>= 1)
+      if ((int64_t)num_seqs * c <= sms) { cs = c; break; }
+  if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
+  // large batches without clusters: 512-thread CTAs, two per SM (MEMSHARE_S1_NT overrides)
+  static int env_nt = -1;
+  if (env_nt < 0) { const char* e = getenv("MEMSHARE_S1_NT"); env_nt = e ? atoi(e) : 0; }
+  const bool half = cs == 1 && (env_nt == 512 || (env_nt == 0 && enc_warp));
+  // the fused fill: stage1 also writes the matches and pairs (offsets from the predecessors'
+  // published counts), so no fill kernel and no last-CTA scan -- offline with the steps as keys,
+  // LAST with the sequences as keys, RANGE with the steps as keys and the current steps as items
+  a.fused = (!half && fused_env() && (cur_mode != MEMSHARE_CUR_LAST || (int64_t)num_seqs <= step_cap + 1)) ? 1 : 0;
+  a.range_items = (cur_mode == MEMSHARE_CUR_RANGE && a.fused) ? 1 : 0;
   if (enc_warp)
     launch_pdl(encode_warp_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
   else
     launch_pdl(encode_kernel, dim3(grid_enc), dim3(kNT), kSmemSlots * sizeof(int2), st, a);
   {
-    // cluster size per current step: online rounds (LAST: one current step per sequence) split
-    // each step's history over up to 8 CTAs while the clusters still fit in one wave; offline
-    // (ALL) and RANGE calls keep one CTA per step. MEMSHARE_S1_CLUSTER overrides the LAST size (tuning).
-    static int env_cs = -1;
-    if (env_cs < 0) { const char* e = getenv("MEMSHARE_S1_CLUSTER"); env_cs = e ? atoi(e) : 0; }
-    int cs = 1;
-    if (env_cs > 0 && cur_mode != MEMSHARE_CUR_ALL) cs = env_cs;    // forced (tuning / regression tests)
-    else if (cur_mode == MEMSHARE_CUR_LAST)
-      for (int c = 8; c > 1; c >>= 1)
-        if ((int64_t)num_seqs * c <= sms) { cs = c; break; }
-    if (cs != 1 && cs != 2 && cs != 4 && cs != 8) cs = 1;
-    // large batches without clusters: 512-thread CTAs, two per SM (MEMSHARE_S1_NT overrides)
-    static int env_nt = -1;
-    if (env_nt < 0) { const char* e = getenv("MEMSHARE_S1_NT"); env_nt = e ? atoi(e) : 0; }
-    const bool half = cs == 1 && (env_nt == 512 || (env_nt == 0 && enc_warp));
     const int per_sm = half ? 2 : 1;
     const int ncl = (int)((gcap < (int64_t)per_sm * sms / cs) ? gcap : (int64_t)per_sm * sms / cs);
     cudaLaunchConfig_t cfg = {};
@@ -1286,13 +1380,8 @@ extern "C" memshare_status memshare_step_candidates(
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    // offline single-CoT shape (one 1024-thread CTA per step, no cluster): stage1 also writes the
-    // matches and pairs (offsets from the predecessors' published counts), so no fill kernel and no last-CTA scan
-    // (online rounds fuse too: RANGE with the steps as keys -- the non-current ones publish
-    // zeros -- and LAST with the sequences as keys, one current step each)
-    a.fused = (!half && fused_env() &&
-               (cur_mode != MEMSHARE_CUR_LAST || (int64_t)num_seqs <= step_cap + 1)) ? 1 : 0;
-    if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : stage1_kernel<1024>, a) != cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, half ? stage1_kernel<512> : (a.range_items ? stage1_kernel<1024, true>
+                                                                            : stage1_kernel<1024>), a) != cudaSuccess)
       return MEMSHARE_ERR_CUDA;
   }
   if (!a.fused) launch_pdl(fill_kernel, dim3(grid_sel), dim3(kNT), sizeof(FillSmem), st, a);
