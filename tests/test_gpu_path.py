@@ -202,6 +202,34 @@ def test_stage_geometries(shape):
     full_parity(w)
 
 
+@pytest.mark.parametrize("case", ["empty", "clamped", "all_steps", "mixed"])
+def test_range_round_work_items(case):
+    """RANGE rounds take the current steps as work items (a dense list built by the encode kernel;
+    zeros published for every other step): all-empty ranges (no item: the totals are written
+    directly), ranges beyond the step counts and negative begins (clamped as the oracle does),
+    ranges covering every step (= the offline round), and a mix -- each the full oracle check,
+    with the 8-CTA clusters of few sequences and one CTA per item for many."""
+    w = workloads.small(SMALL, 3, 2600, seed=9)
+    S = np.diff(oracle_steps(w)["seq_step_off"])
+    if case == "empty":
+        cb, ce = [3, 0, 7], [3, 0, 7]
+    elif case == "clamped":
+        cb, ce = [-5, int(S[1]) - 2, int(S[2]) + 3], [2, int(S[1]) + 40, int(S[2]) + 9]
+    elif case == "all_steps":
+        cb, ce = [0, 0, 0], [int(x) for x in S]
+    else:
+        cb, ce = [1, 0, 5], [2, 0, int(S[2])]
+    p, oc, D, near = full_parity(w, tau_s=0.5, cur_mode=oracle.CUR_RANGE, cb=cb, ce=ce)
+    if case == "empty":
+        assert p.counts()["matches"] == 0 and p.counts()["pairs"] == 0
+    if case == "all_steps":
+        ref = oracle_candidates(w, oracle_steps(w), 0.5)             # the offline (ALL) round
+        assert_candidates_equal(p.read_candidates(), ref)
+    w2 = workloads.small(SMALL, 100, 300, seed=10)                     # many sequences: one CTA per item
+    S2 = np.diff(oracle_steps(w2)["seq_step_off"])
+    full_parity(w2, tau_s=0.5, cur_mode=oracle.CUR_RANGE, cb=[0] * 100, ce=[int(min(x, 2)) for x in S2])
+
+
 def test_online_modes():
     """LAST with 3 sequences runs Stage 1 as 8-CTA clusters per current step (DSMEM sum of the
     ranks' partial dots); RANGE runs one CTA per step."""
