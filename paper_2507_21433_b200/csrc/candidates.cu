@@ -1120,13 +1120,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
         if (fused && crank == 0) publish_nothing(wi);
         continue;
       }
-      s = a.ws.step_seq[g];
+      s = last_mode ? (int32_t)wi : a.ws.step_seq[g];       // LAST: the item is the sequence
       key = wi;
     }
     const int64_t gfirst = a.seq_step_off[s];
     const int64_t S = a.seq_step_off[s + 1] - gfirst;
     s1_item<NT>(a, sm, key, g, s, gfirst, S, fused, nwork, &s_lb);
+    // Every cluster takes exactly one ticket first, so with no more items than clusters every item
+    // is already held: leave without the second ticket round trip (s1_item's last cluster barrier
+    // follows the last DSMEM access, so no rank reads another's shared memory after this point).
     if (range_items && wi == nitems - 1 && crank == 0) publish_zero_range(g + 1, nwork);   // and after the last
+    if (nitems <= (int64_t)(gridDim.x / csize)) break;
   }
   DBG_T(7);
   if (!fused && !(a.dbg_skip & 4) && last_block_done(a.ws.done)) {
