@@ -1,10 +1,12 @@
 // Tuning probe (not part of the product): HBM -> shared memory throughput of a TMA 1-D bulk-copy
 // ring (1 CTA per SM, 1 producer lane, 8 consumer warps that only release the stage) as a
 // function of the bytes per copy, the copies per stage (one mbarrier per stage) and the ring
-// depth. Source addresses are scattered copy-sized slices of a 4 GiB buffer.
+// depth. Source addresses are scattered copy-sized slices of a 4 GiB buffer (argument: another
+// footprint in MiB, e.g. 32 for an L2-resident source).
 // Build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tma_sweep tma_sweep.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -66,26 +68,30 @@ __global__ void __launch_bounds__(288, 1) ring(const uint8_t* buf, size_t nslice
   if (acc == 1234.5f) *sink = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  // optional argument: the source footprint in MiB (default 4096: HBM; e.g. 32: L2-resident, to
+  // measure the L2 -> shared-memory rate the sharing regime's re-staged slices run at)
+  const size_t foot_mb = argc > 1 ? (size_t)atoll(argv[1]) : 4096;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* sink;
   cudaMalloc(&sink, 4);
   const int ring_max = 208 * 1024;
   cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_max + 1024);
-  const size_t bytes = (size_t)4 << 30;
+  const size_t bytes = foot_mb << 20;
   uint8_t* buf;
   cudaMalloc(&buf, bytes);
   cudaMemset(buf, 1, bytes);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int copy : {2048, 4096, 8192, 16384, 32768}) {
+  printf("source footprint %zu MiB\n", foot_mb);
+  for (int copy : {2048, 4096, 8192, 16384, 32768, 65536, 98304}) {
     for (int per_stage : {1, 2, 4}) {
       for (int ring_kb : {64, 128, 208}) {
         const int stage_b = copy * per_stage;
         const int stages = ring_kb * 1024 / stage_b;
-        if (stages < 2 || stages > 64) continue;
+        if (stages < 2 || stages > 64 || stages * stage_b > ring_max) continue;
         const size_t nslices = bytes / copy;
         const size_t total = ((size_t)3 << 30) / copy;       // 3 GiB moved
         for (int w = 0; w < 2; ++w)
