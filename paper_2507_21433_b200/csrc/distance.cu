@@ -303,6 +303,17 @@ __device__ __forceinline__ float2 sub_bf2(uint32_t x, float2 t) {
   return d;
 }
 
+// n + s^2 for both halves of a packed bf16 pair, one mixed-precision FMA each (the bf16 product
+// is exact in fp32, one rounding -- the same value as unpack + fp32 FMA, two fewer ops)
+__device__ __forceinline__ float2 sq_bf2(uint32_t x, float2 n) {
+  float2 r;
+  asm("{\n.reg .b16 lo, hi;\nmov.b32 {lo, hi}, %2;\n"
+      "fma.rn.f32.bf16 %0, lo, lo, %3;\nfma.rn.f32.bf16 %1, hi, hi, %4;\n}\n"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(x), "f"(n.x), "f"(n.y));
+  return r;
+}
+
 template <int KRE, int CW = kConsumerWarps>
 struct StCfg {
   static constexpr int kStageB = KRE * 16 * 32 * CW;
@@ -417,10 +428,11 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
     if (h.w & H_ANCHOR) {
 #pragma unroll
       for (int r = 0; r < KRE; ++r) {
-        const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
-        T[4 * r + 0] = f0; T[4 * r + 1] = f1; T[4 * r + 2] = f2; T[4 * r + 3] = f3;
-        n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
-        n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
+        T[4 * r + 0] = bf2_to_f2(x[r].x); T[4 * r + 1] = bf2_to_f2(x[r].y);
+        T[4 * r + 2] = bf2_to_f2(x[r].z); T[4 * r + 3] = bf2_to_f2(x[r].w);
+        // the squared norm exactly as the source stages form it (same ops, same order)
+        n0 = sq_bf2(x[r].x, n0); n1 = sq_bf2(x[r].y, n1);
+        n0 = sq_bf2(x[r].z, n0); n1 = sq_bf2(x[r].w, n1);
       }
       const float tn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
       if (lane == 0) a.ws.wtn[o] = tn;
@@ -429,13 +441,12 @@ __device__ __forceinline__ void st_eval(const DistArgs& a, int4 h, const uint4 (
       float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
       for (int r = 0; r < KRE; ++r) {
-        const float2 f0 = bf2_to_f2(x[r].x), f1 = bf2_to_f2(x[r].y), f2 = bf2_to_f2(x[r].z), f3 = bf2_to_f2(x[r].w);
         const float2 e0 = sub_bf2(x[r].x, T[4 * r + 0]), e1 = sub_bf2(x[r].y, T[4 * r + 1]);
         const float2 e2 = sub_bf2(x[r].z, T[4 * r + 2]), e3 = sub_bf2(x[r].w, T[4 * r + 3]);
         acc0 = __ffma2_rn(e0, e0, acc0); acc1 = __ffma2_rn(e1, e1, acc1);
         acc0 = __ffma2_rn(e2, e2, acc0); acc1 = __ffma2_rn(e3, e3, acc1);
-        n0 = __ffma2_rn(f0, f0, n0); n1 = __ffma2_rn(f1, f1, n1);
-        n0 = __ffma2_rn(f2, f2, n0); n1 = __ffma2_rn(f3, f3, n1);
+        n0 = sq_bf2(x[r].x, n0); n1 = sq_bf2(x[r].y, n1);
+        n0 = sq_bf2(x[r].z, n0); n1 = sq_bf2(x[r].w, n1);
       }
       const float dd = warp_sum((acc0.x + acc0.y) + (acc1.x + acc1.y));
       const float sn = warp_sum((n0.x + n0.y) + (n1.x + n1.y));
