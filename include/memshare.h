@@ -187,9 +187,10 @@ size_t memshare_segment_steps_workspace_size(int64_t num_tokens, int32_t num_seq
  * Limits (CAPACITY if exceeded): <= 1024 survivors per current step when top_k == 0 or
  *   top_k > 512; <= 4096 full blocks per step.
  * Implementation: current steps are work items taken from an atomic ticket (one CTA, or one
- * thread-block cluster sharing the history scan over DSMEM in online LAST rounds); an item's output
- * offsets are the sum of the counts every earlier item published, so it only ever waits on items
- * running CTAs already hold (a wait beyond 2 s reports CORRUPTION). */
+ * thread-block cluster sharing the history scan over DSMEM in online LAST and RANGE rounds; RANGE
+ * work items are the current steps only, listed by the encode kernel); an item's output offsets
+ * are the sum of the counts every earlier item published, so it only ever waits on items running
+ * CTAs already hold (a wait beyond 2 s reports CORRUPTION). */
 memshare_status memshare_step_candidates(
     const int32_t* tokens, int64_t num_tokens, const int64_t* seq_tok_off, int32_t num_seqs,
     const int64_t* seq_step_off, const int32_t* step_start, const int32_t* step_end, const int32_t* step_nbag,
