@@ -2,7 +2,7 @@
 # 16-sequence c3 batch for the working tree and the old tree in _old/ (see scripts/ab_rev.sh).
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 (cd _old && python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1)
-timeout 900 python -m pytest tests/test_gpu_path.py tests/test_gpu_sanitizer.py -q -x 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_path.py ${SANITIZE:+tests/test_gpu_sanitizer.py} -q -x 2>&1 | tail -2
 A="--config c2 --no-cpu-baseline --no-e2e --no-online --seed-sweep 0,1,2"
 C="--config c3 --batch-seqs 16 --steps 5 --no-cpu-baseline --no-e2e --no-online"
 for i in 1 2; do
