@@ -80,6 +80,12 @@ typedef int32_t memshare_status;
 #define MEMSHARE_DIST_FULL 0
 #define MEMSHARE_DIST_PARTIAL 1
 #define MEMSHARE_DIST_FINALIZE 2
+/* Schedule hint OR'ed into the memshare_block_distance mode (FULL or PARTIAL, Euclidean metric;
+ * ignored otherwise): the list's consecutive targets share their sources -- CROSS pairing, the
+ * all-pairs matrix -- so runs of targets whose source list is a prefix of the next target's are
+ * evaluated together, every shared source slice staged once for up to four targets. Same
+ * definitions and outputs; only the fixed fp32 summation order of the partials differs. */
+#define MEMSHARE_DIST_GROUPED 0x100
 
 /* Stage-2 block metric. EUCLIDEAN is Alg. 1 Stage 2. COSINE is the variant the
  * paper compares against (Fig. 7, reading R34): per layer the cosine of the K
@@ -264,7 +270,8 @@ size_t memshare_remap_workspace_size(int32_t num_blocks, int64_t target_cap);
  *   workspace >= memshare_block_distance_remap_workspace_size() bytes.
  * Implementation: the streaming kernel and the finalisation kernel of memshare_block_distance; the
  * finalisation kernel's last CTA to finish then applies the decisions -- one launch fewer than the
- * two calls. Errors: as memshare_block_distance and memshare_remap. */
+ * two calls. `metric` may carry MEMSHARE_DIST_GROUPED (the schedule hint of
+ * memshare_block_distance's mode). Errors: as memshare_block_distance and memshare_remap. */
 memshare_status memshare_block_distance_remap(
     const memshare_kv_pool* pool_host, const memshare_dims* dims_host, const memshare_block_pair* pairs,
     const int64_t* target_off, const int64_t* num_pairs, const int64_t* num_targets, int64_t pair_cap,

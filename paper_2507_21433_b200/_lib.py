@@ -20,6 +20,7 @@ OK, INVALID_ARGUMENT, CAPACITY, CORRUPTION, CUDA_ERROR = 0, 1, 2, 3, 4
 CUR_ALL, CUR_LAST, CUR_RANGE = 0, 1, 2
 PAIR_ALIGNED, PAIR_CROSS = 0, 1
 DIST_FULL, DIST_PARTIAL, DIST_FINALIZE = 0, 1, 2
+DIST_GROUPED = 0x100       # schedule hint OR'ed into the mode (CROSS / all-pairs lists)
 METRIC_EUCLIDEAN, METRIC_COSINE = 0, 1
 
 MATCH_DTYPE = np.dtype([("seq", "<i4"), ("step", "<i4"), ("cand_step", "<i4"), ("rank", "<i4"), ("cosine", "<f8")])

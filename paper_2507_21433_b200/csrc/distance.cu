@@ -47,7 +47,7 @@ constexpr int kMaxRingStages = 48;
 #define MS_ST_MAXKRE kMaxKre      // tuning: cap on the stage size, in 4 KiB units
 #endif
 
-constexpr int H_STOP = 1, H_ANCHOR = 2, H_PAIR = 4;
+constexpr int H_STOP = 1, H_ANCHOR = 2, H_PAIR = 4, H_SKIP = 8;
 
 // a stage header (one 16-byte shared load for the consumers): {out lo, out hi, bytes, code}
 __device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t code) {
@@ -57,6 +57,7 @@ __device__ __forceinline__ int4 make_hdr(int64_t out, int32_t bytes, int32_t cod
 struct DistWs {
   unsigned int* ticket;
   unsigned int* fin_done;  // finalize CTAs done (memshare_block_distance_remap: the last one remaps)
+  uint8_t* pfx;            // grouped schedule: [target_cap] list(t-1) is a prefix of list(t)
   float* wpart;          // [pair_cap][N][2][n_sub][wstride]  per consumer warp: squared sums of t - s (both metrics)
   float* wsn;            // cosine only: [pair_cap][N][2][n_sub][W] source squared norms
   float* wtn;            // cosine only: [target_cap][N][2][n_sub][W] target squared norms
@@ -72,6 +73,7 @@ DistWs dist_layout(Ws& w, int32_t N, int32_t n_sub, int32_t wstride, int64_t pai
   const bool cosine = metric == MEMSHARE_METRIC_COSINE;
   d.wsn = w.take<float>(cosine ? (size_t)pair_cap * per + 1 : 1);
   d.wtn = w.take<float>(cosine ? (size_t)target_cap * per + 1 : 1);
+  d.pfx = w.take<uint8_t>((size_t)target_cap + 1);
   return d;
 }
 
@@ -104,6 +106,8 @@ struct DistArgs {
   DistWs ws;
   int32_t remap;         // memshare_block_distance_remap: the finalize kernel's last CTA remaps
   RemapArgs rm;
+  int32_t grp_r;         // grouped schedule: anchors per group slot (0: the single-anchor kernel)
+  int32_t lpi_grp;       // grouped schedule: layers per unit
 };
 
 // ------------------------------------------------------------------------- PTX helpers
@@ -564,6 +568,407 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) distance_st_kernel(DistArgs a
   }
 }
 
+// ------------------------------------------------------------------ grouped schedule (f2 CROSS, f3)
+// For lists whose consecutive targets share their sources -- CROSS pairing (every block of step k
+// against the same blocks of its matched steps, "pairwise") and the all-pairs
+// matrix (target j against blocks i < j) -- the single-anchor kernel stages
+// every shared source once per target, and the L2 -> SM delivery of those re-staged slices
+// (~10-11 TB/s on B200) bounds it. Here a unit is (slot of kGrpR consecutive targets, layer
+// chunk): runs of targets whose source list is a prefix of the next target's list form a group,
+// every source of the group's longest list is staged ONCE and evaluated against all the group's
+// anchors whose list reaches it. Anchors stay packed bf16 in registers (kGrpR x 16 regs at
+// 16 KiB stages); the source is unpacked to fp32 once per stage and
+//   e = fma(t_bf16, -1, s) = RN(s - t) = -RN(t - s)
+// (one mixed-precision FMA, SASS FHFMA.BF16 with a half-select of the packed anchor), so e*e and
+// every per-thread chain are bit-identical to the single-anchor kernel's; the partials are per
+// 16 KiB sub-slice instead of per slice (only the fixed cross-warp summation order differs).
+constexpr int kGrpR = 4;
+#ifndef MS_GRP_CW
+#define MS_GRP_CW 8
+#endif
+constexpr int kGrpCW = MS_GRP_CW;                           // consumer warps of the grouped kernel
+constexpr int kGrpStageB = 16384;                           // 16 KiB stages
+constexpr int kGrpMaxKre = kGrpStageB / (16 * 32 * kGrpCW);
+
+// a grouped stage header: {x, y, bytes, code | arg << 8}
+//   anchor: x = first pair index of the anchor's list, arg = number of source stages that follow
+//           the block's kGrpR anchor stages (H_SKIP: an empty stage for an unused slot)
+//   pair:   x = source position q in the group's longest list, arg = mask of the anchors reaching q
+//   y = layer | kv << 9 | sub << 10
+__device__ __forceinline__ int4 make_ghdr(int32_t x, int32_t l, int32_t kv, int32_t sub, int32_t bytes, int32_t code,
+                                          int32_t arg) {
+  return make_int4(x, l | (kv << 9) | (sub << 10), bytes, code | (arg << 8));
+}
+
+// pfx[t] = 1 iff target t-1's source list is a prefix of target t's (same physical sources in the
+// same order; an empty list is a prefix of any). One warp per target. Also zeroes the tickets.
+__global__ void __launch_bounds__(256) grp_prefix_kernel(DistArgs a) {
+  pdl_trigger();
+  TL_SCOPE(5);
+  if (blockIdx.x == 0 && threadIdx.x < 2) a.ws.ticket[threadIdx.x] = 0u;
+  const int64_t T = clamp_count(a.num_targets, a.target_cap);
+  const int64_t P = clamp_count(a.num_pairs, a.pair_cap);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nw) {
+    bool ok = false;
+    if (t > 0) {
+      const int64_t lo0 = __ldcg(a.target_off + t - 1);
+      int64_t hi0 = __ldcg(a.target_off + t);
+      const int64_t lo1 = hi0;
+      int64_t hi1 = __ldcg(a.target_off + t + 1);
+      hi0 = hi0 < P ? hi0 : P;
+      hi1 = hi1 < P ? hi1 : P;
+      const int64_t n0 = hi0 - lo0, n1 = hi1 - lo1;
+      ok = n0 <= n1;
+      if (ok)
+        for (int64_t i = lane; i < n0; i += 32)
+          ok = ok && a.pairs[lo0 + i].source_phys == a.pairs[lo1 + i].source_phys;
+      ok = __all_sync(0xffffffffu, ok);
+    }
+    if (lane == 0) a.ws.pfx[t] = ok ? 1 : 0;
+  }
+}
+
+template <int KRE>
+struct GrpSmem {
+  static constexpr int kStageB = KRE * 16 * 32 * kGrpCW;
+  static constexpr int kNSt = kRingBytes / kStageB < kMaxRingStages ? kRingBytes / kStageB : kMaxRingStages;
+  alignas(128) uint8_t ring[kNSt][kStageB];
+  alignas(16) int4 hdr[kNSt];
+  alignas(8) uint64_t full[kNSt];
+  uint64_t empty[kNSt];
+};
+
+template <int KRE>
+__device__ __forceinline__ void grp_producer(GrpSmem<KRE>& sm, const DistArgs& a, int lane) {
+  constexpr int NS = GrpSmem<KRE>::kNSt;
+  constexpr int SB = GrpSmem<KRE>::kStageB;
+  const int64_t I = clamp_count(a.num_targets, a.target_cap);
+  const int64_t Pn = clamp_count(a.num_pairs, a.pair_cap);
+  const int64_t G = (I + kGrpR - 1) / kGrpR;
+  const int32_t lpi = a.lpi_grp;
+  const int64_t total = G * ((a.N + lpi - 1) / lpi);
+  int stage = 0;
+  uint32_t ph = 0;
+  auto put = [&](int32_t phys, const uint8_t* base, int32_t boff, int32_t bytes, int4 h) {
+    mbar_wait(&sm.empty[stage], ph ^ 1u);
+    sm.hdr[stage] = h;
+    mbar_expect_tx(&sm.full[stage], (uint32_t)bytes);
+    bulk_g2s(sm.ring[stage], base + (int64_t)phys * a.block_stride_b + boff, (uint32_t)bytes, &sm.full[stage]);
+    if (++stage == NS) { stage = 0; ph ^= 1u; }
+  };
+  for (;;) {
+    int64_t u = 0;
+    if (lane == 0) u = (int64_t)atomicAdd(a.ws.ticket, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= total) break;
+    // layer-chunk-major; within a chunk the slots in DESCENDING order: the later targets of CROSS
+    // and all-pairs lists have the longest lists, so the heaviest units start first
+    const int64_t lc = u / G, g = G - 1 - (u - lc * G);
+    // lane r < kGrpR: anchor slot r of the group slot
+    const int64_t t = g * kGrpR + lane;
+    const bool valid = lane < kGrpR && t < I;
+    int32_t lo = 0, np = 0, tphys = 0, pf = 0;
+    if (valid) {
+      const int64_t l0 = __ldcg(a.target_off + t);
+      int64_t h0 = __ldcg(a.target_off + t + 1);
+      if (h0 > Pn) h0 = Pn;
+      lo = (int32_t)l0;
+      np = (int32_t)(h0 > l0 ? h0 - l0 : 0);
+      if (np > 0) tphys = a.pairs[l0].target_phys;
+      pf = a.ws.pfx[t];
+    }
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    const uint32_t pmask = __ballot_sync(0xffffffffu, valid && pf);
+    const int32_t l0 = (int32_t)lc * lpi;
+    const int32_t l1 = (l0 + lpi < a.N) ? l0 + lpi : a.N;
+    int ga = 0;
+    while (ga < kGrpR && ((vmask >> ga) & 1u)) {
+      int gb = ga + 1;
+      while (gb < kGrpR && ((vmask >> gb) & 1u) && ((pmask >> gb) & 1u)) ++gb;
+      // group [ga, gb): the longest list is the last anchor's (prefix chain)
+      const int32_t nmax = __shfl_sync(0xffffffffu, np, gb - 1);
+      const int32_t lomax = __shfl_sync(0xffffffffu, lo, gb - 1);
+      int32_t nr[kGrpR], lr[kGrpR], tp[kGrpR];
+#pragma unroll
+      for (int r = 0; r < kGrpR; ++r) {
+        nr[r] = __shfl_sync(0xffffffffu, np, r);
+        lr[r] = __shfl_sync(0xffffffffu, lo, r);
+        tp[r] = __shfl_sync(0xffffffffu, tphys, r);
+        if (r < ga || r >= gb) nr[r] = 0;
+      }
+      for (int32_t c0 = 0; c0 < nmax; c0 += 64) {
+        const int32_t cn = (nmax - c0) < 64 ? nmax - c0 : 64;
+        const int32_t sa = (lane < cn) ? a.pairs[lomax + c0 + lane].source_phys : 0;
+        const int32_t sb = (lane + 32 < cn) ? a.pairs[lomax + c0 + 32 + lane].source_phys : 0;
+        for (int32_t l = l0; l < l1; ++l)
+          for (int32_t kv = 0; kv < 2; ++kv) {
+            const uint8_t* base = (kv ? a.vbase : a.kbase) + (int64_t)l * a.layer_stride_b;
+            for (int32_t sub = 0; sub < a.n_sub; ++sub) {
+              const int32_t boff = sub * SB;
+              const int32_t bytes = (a.slice_bytes - boff) < SB ? a.slice_bytes - boff : SB;
+              if (lane == 0) {
+                // always kGrpR anchor stages, in slot order (an empty one for a slot outside the
+                // group or without pairs in this chunk), each carrying the number of source
+                // stages that follow: the consumers load anchor r into a fixed register set
+#pragma unroll
+                for (int r = 0; r < kGrpR; ++r) {
+                  if (nr[r] > c0) {
+                    put(checked_phys(a, tp[r]), base, boff, bytes, make_ghdr(lr[r], l, kv, sub, bytes, H_ANCHOR, cn));
+                  } else {
+                    mbar_wait(&sm.empty[stage], ph ^ 1u);
+                    sm.hdr[stage] = make_ghdr(0, 0, 0, 0, 0, H_ANCHOR | H_SKIP, cn);
+                    mbar_arrive(&sm.full[stage]);
+                    if (++stage == NS) { stage = 0; ph ^= 1u; }
+                  }
+                }
+              }
+              for (int32_t q = 0; q < cn; ++q) {
+                const int32_t v = __shfl_sync(0xffffffffu, (q & 32) ? sb : sa, q & 31);
+                if (lane == 0) {
+                  int32_t m = 0;
+#pragma unroll
+                  for (int r = 0; r < kGrpR; ++r) m |= (nr[r] > c0 + q) ? (1 << r) : 0;
+                  put(checked_phys(a, v), base, boff, bytes, make_ghdr(c0 + q, l, kv, sub, bytes, H_PAIR, m));
+                }
+              }
+            }
+          }
+      }
+      ga = gb;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    mbar_wait(&sm.empty[stage], ph ^ 1u);
+    sm.hdr[stage] = make_int4(0, 0, 0, H_STOP);
+    mbar_arrive(&sm.full[stage]);
+  }
+}
+
+// e = RN(s - t) for a packed pair of anchor elements (bf16 halves of `t2`) and two fp32 sources
+__device__ __forceinline__ float2 rsub_bf2(uint32_t t2, float s0, float s1) {
+  float2 d;
+  asm("{\n.reg .b16 lo, hi;\nmov.b32 {lo, hi}, %2;\n"
+      "fma.rn.f32.bf16 %0, lo, %5, %3;\nfma.rn.f32.bf16 %1, hi, %5, %4;\n}\n"
+      : "=f"(d.x), "=f"(d.y)
+      : "r"(t2), "f"(s0), "f"(s1), "h"((unsigned short)0xBF80u));
+  return d;
+}
+
+#ifndef MS_GRP_F32
+#define MS_GRP_F32 1
+#endif
+#if MS_GRP_F32
+// anchors held NEGATED in fp32 (the consumer warpgroups own 216 registers, setmaxnreg): e = s + (-t)
+// = RN(s - t) by one FADD2 per two elements, the same value as the FHFMA form
+template <int KRE>
+using GrpAnchor = float2[kGrpR][KRE * 4];
+#else
+template <int KRE>
+using GrpAnchor = uint4[kGrpR][KRE];
+#endif
+
+template <int KRE>
+__device__ __forceinline__ void grp_eval(const DistArgs& a, int4 h, const uint4 (&x)[KRE],
+                                         const GrpAnchor<KRE>& A, const int32_t (&lo)[kGrpR], int warp,
+                                         int lane) {
+  const int arg = h.w >> 8;
+#ifdef MS_DIST_NOEVAL
+  {  // tuning only: the pipeline without the arithmetic (the loaded words are folded)
+    uint32_t f = 0u;
+#pragma unroll
+    for (int c = 0; c < KRE; ++c) f ^= x[c].x ^ x[c].y ^ x[c].z ^ x[c].w;
+    if (f == 0x9E3779B9u) a.ws.wpart[(int64_t)lo[0] + h.x + warp] = 1.f;
+    return;
+  }
+#endif
+  float2 acc[kGrpR][2];
+#pragma unroll
+  for (int r = 0; r < kGrpR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
+  // the source chunk is unpacked once and used by every anchor
+  auto chunk = [&](int c, int r, const float2& s0, const float2& s1, const float2& s2, const float2& s3) {
+#if MS_GRP_F32
+    const float2 e0 = __fadd2_rn(s0, A[r][4 * c + 0]), e1 = __fadd2_rn(s1, A[r][4 * c + 1]);
+    const float2 e2 = __fadd2_rn(s2, A[r][4 * c + 2]), e3 = __fadd2_rn(s3, A[r][4 * c + 3]);
+#else
+    const float2 e0 = rsub_bf2(A[r][c].x, s0.x, s0.y), e1 = rsub_bf2(A[r][c].y, s1.x, s1.y);
+    const float2 e2 = rsub_bf2(A[r][c].z, s2.x, s2.y), e3 = rsub_bf2(A[r][c].w, s3.x, s3.y);
+#endif
+    acc[r][0] = __ffma2_rn(e0, e0, acc[r][0]);
+    acc[r][1] = __ffma2_rn(e1, e1, acc[r][1]);
+    acc[r][0] = __ffma2_rn(e2, e2, acc[r][0]);
+    acc[r][1] = __ffma2_rn(e3, e3, acc[r][1]);
+  };
+  if (arg == (1 << kGrpR) - 1) {
+    // every anchor reaches this source (the common case): one straight-line block, so the
+    // scheduler interleaves the four anchors' independent FHFMA / FFMA2 chains
+#pragma unroll
+    for (int c = 0; c < KRE; ++c) {
+      const float2 s0 = bf2_to_f2(x[c].x), s1 = bf2_to_f2(x[c].y), s2 = bf2_to_f2(x[c].z), s3 = bf2_to_f2(x[c].w);
+#pragma unroll
+      for (int r = 0; r < kGrpR; ++r) chunk(c, r, s0, s1, s2, s3);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < KRE; ++c) {
+      const float2 s0 = bf2_to_f2(x[c].x), s1 = bf2_to_f2(x[c].y), s2 = bf2_to_f2(x[c].z), s3 = bf2_to_f2(x[c].w);
+#pragma unroll
+      for (int r = 0; r < kGrpR; ++r)
+        if (arg & (1 << r)) chunk(c, r, s0, s1, s2, s3);
+    }
+  }
+  const int32_t l = h.y & 511, kv = (h.y >> 9) & 1, sub = h.y >> 10;
+  // the four anchors' warp sums in one transposed butterfly (6 shuffles instead of 20): after the
+  // xor-16 and xor-8 exchanges lane group (lane >> 3) carries anchor (lane >> 3)'s partial
+  static_assert(kGrpR == 4, "transposed reduction is written for four anchors");
+  float v[kGrpR];
+#pragma unroll
+  for (int r = 0; r < kGrpR; ++r) v[r] = (acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y);
+  const bool b4 = lane & 16, b3 = lane & 8;
+  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
+  const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  float k = b3 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  const int r = lane >> 3;
+  if ((lane & 7) == 0 && (arg & (1 << r))) {
+    int32_t lr = lo[0];
+#pragma unroll
+    for (int i = 1; i < kGrpR; ++i) lr = r == i ? lo[i] : lr;
+    const int64_t p = (int64_t)lr + h.x;
+    a.ws.wpart[(((p * a.N + l) * 2 + kv) * a.n_sub + sub) * a.wstride + warp] = k;
+  }
+}
+
+#if MS_GRP_F32
+constexpr int kGrpThreads = kGrpCW * 32 + 128;             // + one producer WARPGROUP (setmaxnreg)
+#else
+constexpr int kGrpThreads = kGrpCW * 32 + 32;
+#endif
+
+template <int KRE, bool PARTIAL>
+__global__ void __launch_bounds__(kGrpThreads, 1) distance_grp_kernel(DistArgs a) {
+  constexpr int NS = GrpSmem<KRE>::kNSt;
+  constexpr int NC = kGrpCW * 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  GrpSmem<KRE>& sm = *reinterpret_cast<GrpSmem<KRE>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kGrpCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  TL_SCOPE(6);
+#if MS_GRP_F32
+  // register reconfiguration (whole warpgroups): the producer warpgroup gives its registers to the
+  // two consumer warpgroups (4 x 32 x 64 + 8 x 32 x 216 <= the 384 x 168 allocated at launch)
+  if (warp >= kGrpCW) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+    if (warp == kGrpCW) grp_producer<KRE>(sm, a, lane);
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+#else
+  if (warp == kGrpCW) {
+    grp_producer<KRE>(sm, a, lane);
+    return;
+  }
+#endif
+  GrpAnchor<KRE> A;
+  int32_t lo[kGrpR];
+#pragma unroll
+  for (int r = 0; r < kGrpR; ++r) lo[r] = 0;
+  uint4 xa[KRE], xb[KRE];
+  int stage = 0;
+  uint32_t ph = 0;
+  auto load = [&](uint4 (&dst)[KRE], int32_t bytes) {
+    const uint4* src = reinterpret_cast<const uint4*>(sm.ring[stage]);
+    if (!PARTIAL || bytes == GrpSmem<KRE>::kStageB) {
+#pragma unroll
+      for (int r = 0; r < KRE; ++r) dst[r] = src[tid + r * NC];
+    } else {
+      const int nchunk = bytes >> 4;
+#pragma unroll
+      for (int r = 0; r < KRE; ++r) {
+        const int c = tid + r * NC;
+        dst[r] = c < nchunk ? src[c] : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (++stage == NS) { stage = 0; ph ^= 1u; }
+  };
+  // A block = kGrpR anchor stages (fixed slots -> fixed registers) + the source stages; the inner
+  // loop never writes the anchors, so no register shuffling at its head (a single loop with the
+  // anchor update inside made ~30 % of the instructions moves). Eight consumer warps hide each
+  // other's shared-memory load latency.
+  for (;;) {
+    int32_t n = 0;
+#pragma unroll
+    for (int r = 0; r < kGrpR; ++r) {
+      mbar_wait(&sm.full[stage], ph);
+      const int4 h = sm.hdr[stage];
+      if (r == 0 && (h.w & H_STOP)) return;
+      if (!(h.w & H_SKIP)) {
+#if MS_GRP_F32
+        load(xa, h.z);
+#pragma unroll
+        for (int c = 0; c < KRE; ++c) {
+          const uint32_t w4[4] = {xa[c].x, xa[c].y, xa[c].z, xa[c].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            A[r][4 * c + j] = make_float2(__uint_as_float((w4[j] << 16) ^ 0x80000000u),
+                                          __uint_as_float((w4[j] & 0xFFFF0000u) ^ 0x80000000u));
+        }
+#else
+        load(A[r], h.z);
+#endif
+        lo[r] = h.x;
+      }
+      n = h.w >> 8;
+      release();
+    }
+    // the source stages, ping-pong: the next stage is copied to registers before this one is
+    // evaluated (two evaluation sites; the anchors are read-only here, so no shuffling)
+    int4 ha, hb;
+    mbar_wait(&sm.full[stage], ph);
+    ha = sm.hdr[stage];
+    load(xa, ha.z);
+    release();
+    for (int32_t q = 0;; q += 2) {
+      if (q + 1 < n) {
+        mbar_wait(&sm.full[stage], ph);
+        hb = sm.hdr[stage];
+        load(xb, hb.z);
+        release();
+      }
+      grp_eval<KRE>(a, ha, xa, A, lo, warp, lane);
+      if (q + 1 >= n) break;
+      if (q + 2 < n) {
+        mbar_wait(&sm.full[stage], ph);
+        ha = sm.hdr[stage];
+        load(xa, ha.z);
+        release();
+      }
+      grp_eval<KRE>(a, hb, xb, A, lo, warp, lane);
+      if (q + 2 >= n) break;
+    }
+  }
+}
+
 // Finalisation: one CTA per target (grid-stride). FULL/PARTIAL read the per-warp partials the
 // streaming kernel left in the workspace (kernel boundary = the only synchronisation needed);
 // FINALIZE reads partial squared sums already reduced across ranks.
@@ -604,6 +1009,16 @@ static int st_maxk() {
   return v;
 }
 
+// grouped schedule: stages of <= kGrpMaxKre x 4 KiB for eight consumer warps
+static int grp_geometry(int64_t slice_bytes, int32_t* n_sub) {
+  constexpr int64_t unit = 16 * 32 * kGrpCW;           // one 16-byte chunk per consumer thread
+  const int64_t units = (slice_bytes + unit - 1) / unit;
+  const int64_t ns = (units + kGrpMaxKre - 1) / kGrpMaxKre;
+  *n_sub = (int32_t)(ns < 1 ? 1 : ns);
+  const int64_t kre = (units + *n_sub - 1) / *n_sub;
+  return (int)(kre < 1 ? 1 : kre);
+}
+
 static int st_geometry(int64_t slice_bytes, int32_t* n_sub, int32_t* cw = nullptr) {
   if (cw) *cw = kConsumerWarps;
   if (slice_bytes == kPhi4Slice && st_maxk() >= 8) {   // one 40 KiB stage, ten consumer warps x 8 chunks
@@ -636,6 +1051,38 @@ static cudaError_t launch_st(const DistArgs& a, cudaStream_t st) {
 
 // PARTIAL: the slice is not a whole number of stages (its last stage is partial); only those
 // instantiations carry the predicated loads (they cost ~10 % on L2-heavy lists otherwise)
+template <int KRE, bool PARTIAL>
+static cudaError_t launch_grp(const DistArgs& a, cudaStream_t st) {
+  static bool attr_set_dev[kMaxDevices] = {};
+  bool& attr_set = attr_set_dev[current_device()];
+  if (!attr_set) {
+    const cudaError_t e = cudaFuncSetAttribute(distance_grp_kernel<KRE, PARTIAL>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sizeof(GrpSmem<KRE>));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  return launch_pdl(distance_grp_kernel<KRE, PARTIAL>, dim3(sm_count()), dim3(kGrpThreads),
+                    sizeof(GrpSmem<KRE>), st, a);
+}
+
+static cudaError_t launch_grp_any(int kre, bool partial, const DistArgs& a, cudaStream_t st) {
+  static_assert(kGrpMaxKre <= 4, "instantiate the larger grouped stages");
+  switch (kre * 2 + (partial ? 1 : 0)) {
+    case 2: return launch_grp<1, false>(a, st);
+    case 3: return launch_grp<1, true>(a, st);
+    case 4: return launch_grp<2, false>(a, st);
+    case 5: return launch_grp<2, true>(a, st);
+#if MS_GRP_CW <= 8
+    case 6: return launch_grp<3, false>(a, st);
+    case 7: return launch_grp<3, true>(a, st);
+    case 8: return launch_grp<4, false>(a, st);
+    case 9: return launch_grp<4, true>(a, st);
+#endif
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int MET, bool PARTIAL>
 static cudaError_t launch_st_kre(int kre, const DistArgs& a, cudaStream_t st) {
   switch (kre) {
@@ -688,7 +1135,12 @@ extern "C" size_t memshare_block_distance_workspace_size(const memshare_dims* di
   st_geometry(slice, &n_sub, &cw);
   Ws w{nullptr, 0};
   dist_layout(w, dims->num_layers, n_sub, (cw + 3) / 4 * 4, pair_cap, target_cap, metric);
-  return w.size();
+  // the grouped schedule (MEMSHARE_DIST_GROUPED) keeps partials per 16 KiB sub-slice
+  int32_t g_sub = 1;
+  grp_geometry(slice, &g_sub);
+  Ws wg{nullptr, 0};
+  dist_layout(wg, dims->num_layers, g_sub, (kGrpCW + 3) / 4 * 4, pair_cap, target_cap, metric);
+  return w.size() > wg.size() ? w.size() : wg.size();
 }
 
 static memshare_status block_distance_impl(const memshare_kv_pool* pool, const memshare_dims* dims,
@@ -702,6 +1154,8 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
                                                    const RemapArgs* rm) {
   if (!dims || !pairs || !target_off || !num_pairs || !num_targets || !workspace || !device_status)
     return MEMSHARE_ERR_INVALID_ARGUMENT;
+  const bool grouped_hint = (mode & MEMSHARE_DIST_GROUPED) != 0;
+  mode &= ~MEMSHARE_DIST_GROUPED;
   if (mode < MEMSHARE_DIST_FULL || mode > MEMSHARE_DIST_FINALIZE) return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (metric != MEMSHARE_METRIC_EUCLIDEAN && metric != MEMSHARE_METRIC_COSINE) return MEMSHARE_ERR_INVALID_ARGUMENT;
   if (metric == MEMSHARE_METRIC_COSINE && mode != MEMSHARE_DIST_FULL) return MEMSHARE_ERR_INVALID_ARGUMENT;
@@ -738,7 +1192,18 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
   a.num_blocks = num_blocks;
   a.N = dm.num_layers; a.d = dm.block_size; a.h_global = dm.num_kv_heads_global;
   a.slice_bytes = (int32_t)slice_bytes;
-  const int kre = st_geometry(slice_bytes, &a.n_sub, &a.cw);
+  // the grouped schedule serves the Euclidean metric (the cosine metric keeps the single-anchor
+  // kernel: it needs the source norms per pair)
+  const bool grouped = grouped_hint && metric == MEMSHARE_METRIC_EUCLIDEAN && mode != MEMSHARE_DIST_FINALIZE;
+  int kre;
+  if (grouped) {
+    kre = grp_geometry(slice_bytes, &a.n_sub);
+    a.cw = kGrpCW;
+    a.grp_r = kGrpR;
+    a.lpi_grp = 1;                                   // 1-layer units: finer tail balance
+  } else {
+    kre = st_geometry(slice_bytes, &a.n_sub, &a.cw);
+  }
   a.wstride = (a.cw + 3) / 4 * 4;
   static int lpi_env = -1;
   if (lpi_env < 0) {
@@ -769,11 +1234,16 @@ static memshare_status block_distance_impl(const memshare_kv_pool* pool, const m
     launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 1);
     return launch_status();
   }
-  launch_pdl(ticket_reset_kernel, dim3(1), dim3(32), 0, st, a.ws.ticket);
+  if (grouped) {
+    const int64_t tw = (tc + 7) / 8;                 // a warp per target, 8 per CTA
+    launch_pdl(grp_prefix_kernel, dim3((unsigned)(tw < 4 * sm_count() ? tw : 4 * sm_count())), dim3(256), 0, st, a);
+  } else {
+    launch_pdl(ticket_reset_kernel, dim3(1), dim3(32), 0, st, a.ws.ticket);
+  }
   const bool prof = g_prof_begin != nullptr && g_prof_end != nullptr;
   if (prof && cudaEventRecord(g_prof_begin, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   const bool partial = slice_bytes % ((int64_t)kre * 16 * 32 * a.cw) != 0;
-  const cudaError_t le = launch_st_any(kre, partial, metric, a, st);
+  const cudaError_t le = grouped ? launch_grp_any(kre, partial, a, st) : launch_st_any(kre, partial, metric, a, st);
   if (le != cudaSuccess) return MEMSHARE_ERR_CUDA;
   if (prof && cudaEventRecord(g_prof_end, st) != cudaSuccess) return MEMSHARE_ERR_CUDA;
   launch_pdl(finalize_kernel, dim3(fin_grid), dim3(kFinThreads), 0, st, a, 0);
@@ -812,8 +1282,11 @@ extern "C" memshare_status memshare_block_distance_remap(
     return MEMSHARE_ERR_INVALID_ARGUMENT;
   const RemapArgs rm{block_table, table_stride, num_seqs, refcount, pool->num_blocks, free_list, free_count, decisions,
                      num_targets, target_cap, block_size, num_freed, affected_tokens, RemapWs{}, device_status};
+  // the grouped schedule hint travels in the metric argument here (this call has no mode)
+  const int32_t hint = metric & MEMSHARE_DIST_GROUPED;
+  metric &= ~MEMSHARE_DIST_GROUPED;
   return block_distance_impl(pool, dims, pairs, target_off, num_pairs, num_targets, pair_cap, target_cap,
-                             MEMSHARE_DIST_FULL, metric, nullptr, tau_b, distance, under, decisions, workspace,
+                             MEMSHARE_DIST_FULL | hint, metric, nullptr, tau_b, distance, under, decisions, workspace,
                              workspace_bytes, device_status, stream, &rm);
 }
 

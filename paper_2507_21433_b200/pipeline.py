@@ -10,6 +10,8 @@ tests and reporting only.
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -170,6 +172,8 @@ class MemSharePath:
         cb = None if cur_begin is None else _dev_i32(cur_begin, self.dev)
         ce = None if cur_end is None else _dev_i32(cur_end, self.dev)
         self._cur_keep = (cb, ce)
+        # CROSS lists: the targets of a step share their sources -> the grouped distance schedule
+        self.grouped_hint = pairing == L.PAIR_CROSS
         L.check(L.step_candidates(self.tokens, self.num_tokens, self.seq_tok_off, self.num_seqs, self.seq_step_off,
                                   self.step_start, self.step_end, self.step_nbag, self.caps.step, self.delims, cur_mode,
                                   cb, ce, self.table, self.table_stride, self.num_blocks, self.block_size, tau_s, top_k,
@@ -179,6 +183,8 @@ class MemSharePath:
 
     def distance_call(self, tau_b, mode=L.DIST_FULL, partial_sq=None, metric=L.METRIC_EUCLIDEAN):
         ps = partial_sq if partial_sq is not None else self.partial_sq
+        if mode != L.DIST_FINALIZE:
+            mode |= self._grouped(metric)
         L.check(L.block_distance(None if mode == L.DIST_FINALIZE else self.pool, self.dims, self.pairs,
                                  self.target_off, self.num_pairs, self.num_targets, self.caps.pair, self.caps.target,
                                  mode, ps, tau_b, self.distance, self.under, self.decisions, self.workspace,
@@ -196,11 +202,22 @@ class MemSharePath:
                         self.free_count, self.decisions, self.num_targets, self.caps.target, self.block_size,
                         self.num_freed, self.affected, self.workspace, self.status, self.stream), "remap")
 
+    def _grouped(self, metric):
+        """MEMSHARE_DIST_GROUPED for lists whose targets share sources (CROSS, all-pairs; Euclidean
+        metric) when MEMSHARE_GROUPED=1. Off by default: on B200 the grouped schedule halves the
+        staging cost but the consumer arithmetic bounds both schedules, and it measured slower
+        (profiles/r1_tuning_log.md, "Grouped schedule")."""
+        if (getattr(self, "grouped_hint", False) and metric == L.METRIC_EUCLIDEAN
+                and os.environ.get("MEMSHARE_GROUPED", "0") == "1"):
+            return L.DIST_GROUPED
+        return 0
+
     def distance_remap(self, tau_b, metric=L.METRIC_EUCLIDEAN):
         """a5-a7 as one call: distance_call(FULL) + remap() with the finalisation and the remap fused
         into the streaming kernel (identical results)."""
         L.check(L.block_distance_remap(self.pool, self.dims, self.pairs, self.target_off, self.num_pairs,
-                                       self.num_targets, self.caps.pair, self.caps.target, metric, tau_b,
+                                       self.num_targets, self.caps.pair, self.caps.target,
+                                       metric | self._grouped(metric), tau_b,
                                        self.distance, self.under, self.decisions, self.table, self.table_stride,
                                        self.num_seqs, self.refcount, self.free_list, self.free_count,
                                        self.block_size, self.num_freed, self.affected, self.workspace, self.status,
@@ -220,6 +237,7 @@ class MemSharePath:
         distance_call() scores the distance matrix). Caps must hold sum m(m-1)/2 pairs."""
         bb, be = _dev_i32(blk_begin, self.dev), _dev_i32(blk_end, self.dev)
         self._ap_keep = (bb, be)
+        self.grouped_hint = True          # target j's sources are blocks lo..j-1: nested prefixes
         ws = torch.empty(max(1, L.all_pairs_workspace_size(self.num_seqs)), dtype=torch.uint8, device=self.dev)
         self._ap_ws = ws
         L.check(L.all_pairs(self.seq_tok_off, self.num_seqs, bb, be, self.table, self.table_stride, self.num_blocks,
