@@ -798,7 +798,30 @@ def live_copy_gbs(dev):
     return 2 * 2 * (1 << 30) / (best / 1e3) / 1e9
 
 
-def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_name, live=None):
+# L2 -> shared-memory delivery of a TMA ring with 32 KiB copies (one per stage) from an L2-resident
+# source on this pool's B200: 16.2-16.7 TB/s (scripts/tma_sweep.cu 32, lean producer; 19.4 TB/s
+# with 64 KiB copies), profiles/r1_tuning_log.md "L2 -> SM delivery ceiling"
+L2_DELIVERY_GBS = 16500.0
+
+
+def dual_ceiling(U, T, P, kv_bytes, d_ms):
+    """The distance kernel stages T + P slices per (layer, K|V) (each target once, each pair's source
+    once) of which U are distinct: its time is bounded by max(distinct bytes / HBM peak, staged bytes
+    / L2 delivery ceiling). Returns the staged bytes, the L2-delivery fraction and the fraction of the
+    larger of the two bounds."""
+    peak, _ = measured_peaks()
+    per_block = kv_bytes / max(U, 1)
+    staged = (T + P) * per_block
+    t_hbm = kv_bytes / (peak * 1e9)
+    t_l2 = staged / (L2_DELIVERY_GBS * 1e9)
+    return {"staged_bytes": staged, "staged_over_distinct": (T + P) / max(U, 1),
+            "l2_delivery_gbs": staged / (d_ms / 1e3) / 1e9, "l2_delivery_peak_gbs": L2_DELIVERY_GBS,
+            "l2_frac": staged / (d_ms / 1e3) / 1e9 / L2_DELIVERY_GBS,
+            "bound": "l2_delivery" if t_l2 > t_hbm else "hbm",
+            "frac_of_bound": max(t_hbm, t_l2) / (d_ms / 1e3)}
+
+
+def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_name, live=None, T=None):
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / (d_ms / 1e3) / 1e9
     r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -819,6 +842,12 @@ def roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P, traffic, kernel_na
     if live:
         r["live_copy_gbs"] = live
         r["frac_of_live_copy"] = achieved / live
+    if T is not None:
+        r["dual"] = dual_ceiling(U, T, P, kv_bytes, d_ms)
+        r["dual"]["note"] = ("the HBM fraction counts distinct bytes; the kernel also re-stages shared sources "
+                             "from L2 (T+P slices per layer and K|V): staged bytes against the TMA L2 -> smem "
+                             "rate of 32 KiB copies (16.5 TB/s, scripts/tma_sweep.cu); the larger of the two "
+                             "times is the kernel's bound")
     return r
 
 
@@ -904,7 +933,7 @@ def run_single(args, rank, world, local):
         "roofline": roofline(alg_bytes, d_ms, kernel_only_ms, kv_bytes, U, P,
                              committed_traffic(args.config, f"{args.config}_seed{args.seed}"),
                              "distance_st_kernel (memshare_block_distance_remap)" if r.fused
-                             else "distance_st_kernel (memshare_block_distance)", live=live_copy_gbs(dev)),
+                             else "distance_st_kernel (memshare_block_distance)", live=live_copy_gbs(dev), T=T),
         "per_step": {"pairs": P, "targets": T, "steps": r.counts["steps"], "matches": r.counts["matches"],
                      "freed_blocks": step_freed, "affected_tokens": step_affected},
         "gpu_launches": gpu_launches_per_step(w.num_tokens, torch.cuda.get_device_properties(dev).multi_processor_count,
@@ -927,17 +956,21 @@ def seed_sweep(args, dev, seeds, dist):
         w = workloads.c2(seed=sd)
         r = Run(w, dev, args, 1, 0, "seq", dist)
         r.prepare()
-        alg, U, _ = r.alg_bytes()
+        alg, U, kvb = r.alg_bytes()
         clocks = ClockSampler(dev.index or 0)
         ms, d_ms = r.timed(clocks)
         clocks.stop()
         per.append({"seed": sd, "pairs": r.counts["pairs"], "targets": r.counts["targets"], "distinct_blocks": U,
                     "ms_per_step": ms, "pairs_per_s": r.counts["pairs"] / (ms / 1e3),
-                    "distance_frac": alg / (d_ms / 1e3) / 1e9 / measured_peaks()[0]})
+                    "distance_frac": alg / (d_ms / 1e3) / 1e9 / measured_peaks()[0],
+                    "dual": dual_ceiling(U, r.counts["targets"], r.counts["pairs"], kvb, d_ms)})
         r.free()
     st = lambda k: {"mean": float(np.mean([x[k] for x in per])), "min": float(min(x[k] for x in per)),
                     "max": float(max(x[k] for x in per))}
-    return {"seeds": seeds, "pairs_per_s": st("pairs_per_s"), "distance_frac": st("distance_frac"), "per_seed": per}
+    fb = [x["dual"]["frac_of_bound"] for x in per]
+    return {"seeds": seeds, "pairs_per_s": st("pairs_per_s"), "distance_frac": st("distance_frac"),
+            "frac_of_dual_bound": {"mean": float(np.mean(fb)), "min": float(min(fb)), "max": float(max(fb))},
+            "per_seed": per}
 
 
 # ----------------------------------------------------------------------------- our arm: a partitioned batch
@@ -1046,6 +1079,7 @@ def run_batch(args, rank, world, local):
         waves.append({"rank": rank, "wave": wi, "seqs": len(idx), "tokens": w.num_tokens, "pairs": c["pairs"],
                       "targets": c["targets"], "distinct_blocks": U, "ms_per_step": m, "distance_ms": d_ms,
                       "kernel_only_ms": k_ms, "distance_frac": alg / (d_ms / 1e3) / 1e9 / measured_peaks()[0],
+                      "dual": dual_ceiling(U, c["targets"], c["pairs"], kvb, d_ms),
                       "e2e_ms_per_step": wave_e2e, "parity": par, "pool_gb": w.pool_bytes() / 1e9})
         r.free()
         del r, w
@@ -1088,7 +1122,8 @@ def run_batch(args, rank, world, local):
         "roofline": roofline(tot["alg"], tot["d_ms"], tot["k_ms"], tot["kv"], tot["U"], tot["pairs"],
                              committed_traffic(cfg, f"{cfg}_{n}seq_{world}gpu_seed{args.seed}"),
                              "distance_st_kernel (memshare_block_distance_remap)" if fused_tail
-                             else "distance_st_kernel (memshare_block_distance)", live=live_copy_gbs(dev)),
+                             else "distance_st_kernel (memshare_block_distance)", live=live_copy_gbs(dev),
+                             T=tot["targets"]),
         "per_step": {"pairs": int(pairs_all), "pairs_rank0": tot["pairs"], "targets_rank0": tot["targets"],
                      "steps_rank0": tot["steps"], "matches_rank0": tot["matches"], "freed_blocks_rank0": tot["freed"],
                      "affected_tokens_rank0": tot["affected"]},

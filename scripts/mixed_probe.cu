@@ -23,7 +23,7 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
 }
 
 __global__ void __launch_bounds__(288, 1) mixed(const uint8_t* hbm, size_t n_hbm, const uint8_t* l2, size_t n_l2,
-                                                int H, int M, int route, size_t stages_total, float* sink, int consume) {
+                                                int H, int M, int route, size_t stages_total, float* sink, int consume, unsigned long long mult) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + 16;
@@ -38,12 +38,15 @@ __global__ void __launch_bounds__(288, 1) mixed(const uint8_t* hbm, size_t n_hbm
   }
   __syncthreads();
   if (warp == 8) {
+    if (route == 0 && lane != 0) return;               // all-TMA: one producer lane, as tma_sweep.cu
     int st = 0;
     uint32_t ph = 0;
     int nl2 = 0;
     for (size_t i = blockIdx.x, k = 0; i < stages_total; i += gridDim.x, ++k) {
+      // lean address math (power-of-two slice counts: a mask, no 64-bit modulo)
       const bool from_hbm = (int)(k % M) < H;
-      const uint8_t* src = from_hbm ? hbm + ((i * 7919ull) % n_hbm) * kSlice : l2 + ((i * 131ull) % n_l2) * kSlice;
+      const uint8_t* src = from_hbm ? hbm + (size_t)((uint32_t)(i * 7919u) & (uint32_t)(n_hbm - 1)) * kSlice
+                                    : l2 + (size_t)((uint32_t)(i * (uint32_t)mult) & (uint32_t)(n_l2 - 1)) * kSlice;
       const bool lsu = !from_hbm && (route == 1 || (route == 2 && (nl2++ & 1)));
       uint8_t* dst = data + (size_t)st * kSlice;
       if (!lsu) {
@@ -56,7 +59,7 @@ __global__ void __launch_bounds__(288, 1) mixed(const uint8_t* hbm, size_t n_hbm
               "l"(src), "r"(kSlice), "r"(smem_u32(full + st))
               : "memory");
         }
-        __syncwarp();
+        if (route != 0) __syncwarp();
       } else {
         wait(empty + st, ph ^ 1u);
 #pragma unroll 8
@@ -91,14 +94,16 @@ __global__ void __launch_bounds__(288, 1) mixed(const uint8_t* hbm, size_t n_hbm
   if (acc == 1234.5f) *sink = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  // optional: "sweep" = pure-L2 delivery for several slice-index strides and L2 footprints only
+  const bool sweep = argc > 1;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* sink;
   cudaMalloc(&sink, 4);
   const int smem = kStages * kSlice + 1024;
   cudaFuncSetAttribute(mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const size_t hbm_b = (size_t)4 << 30, l2_b = (size_t)32 << 20;
+  const size_t hbm_b = (size_t)4 << 30, l2_b = (size_t)96 << 20;
   uint8_t *hbm, *l2;
   cudaMalloc(&hbm, hbm_b);
   cudaMalloc(&l2, l2_b);
@@ -108,16 +113,34 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const size_t total = ((size_t)4 << 30) / kSlice;          // 4 GiB delivered per run
-  struct P { int H, M; } pats[] = {{1, 1}, {0, 1}, {3, 4}, {1, 2}, {3, 8}, {1, 3}, {1, 4}};
+  struct P { int H, M; } pats[] = {{1, 1}, {0, 1}, {3, 4}, {5, 9}, {1, 2}, {3, 8}, {1, 3}, {1, 4}};
+  if (sweep) {
+    for (size_t foot_mb : {8, 16, 32, 64, 96})
+      for (unsigned long long mult : {1ull, 131ull, 7919ull}) {
+        const size_t n_l2 = (foot_mb << 20) / kSlice;
+        for (int w = 0; w < 2; ++w)
+          mixed<<<sms, 288, smem>>>(hbm, hbm_b / kSlice, l2, n_l2, 0, 1, 0, total, sink, 0, mult);
+        cudaEventRecord(a);
+        mixed<<<sms, 288, smem>>>(hbm, hbm_b / kSlice, l2, n_l2, 0, 1, 0, total, sink, 0, mult);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("pure L2: footprint %3zu MiB, slice stride %5llu: %7.0f GB/s\n", foot_mb, mult,
+               (double)total * kSlice / (ms * 1e6));
+      }
+    printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
   for (int consume = 0; consume < 3; ++consume)
   for (const P& p : pats)
     for (int route = 0; route < 3; ++route) {
       if (p.H == p.M && route > 0) continue;
       if (consume > 0 && route > 0) continue;
       for (int w = 0; w < 2; ++w)
-        mixed<<<sms, 288, smem>>>(hbm, hbm_b / kSlice, l2, l2_b / kSlice, p.H, p.M, route, total, sink, consume);
+        mixed<<<sms, 288, smem>>>(hbm, hbm_b / kSlice, l2, ((size_t)32 << 20) / kSlice, p.H, p.M, route, total, sink, consume, 131ull);
       cudaEventRecord(a);
-      mixed<<<sms, 288, smem>>>(hbm, hbm_b / kSlice, l2, l2_b / kSlice, p.H, p.M, route, total, sink, consume);
+      mixed<<<sms, 288, smem>>>(hbm, hbm_b / kSlice, l2, ((size_t)32 << 20) / kSlice, p.H, p.M, route, total, sink, consume, 131ull);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
