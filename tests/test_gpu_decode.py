@@ -52,17 +52,26 @@ def run_attention(L, pool_k, pool_v, ls, bs, nb, shape, layer, q_bits, hq, table
     return out.cpu().numpy().astype(np.float64)
 
 
-@pytest.mark.parametrize("shape,hq", [(kv.KVShape(3, 8, 128, 16), 40), (kv.KVShape(2, 2, 64, 16), 8),
-                                      (kv.KVShape(2, 10, 128, 16), 40)])
-def test_attention_vs_oracle_ragged(shape, hq):
-    """Ragged lengths (0, 1, d-1, d, d+1, 255-257 chunk edges, random up to 3000) through a shuffled
-    block table; GQA groups of 5, 4 and 4."""
+@pytest.mark.parametrize("shape,hq,S,maxlen", [(kv.KVShape(3, 8, 128, 16), 40, 12, 3000),
+                                                (kv.KVShape(2, 2, 64, 16), 8, 12, 3000),
+                                                (kv.KVShape(2, 10, 128, 16), 40, 12, 3000),
+                                                # enough split CTAs for 32-block (512-token) and
+                                                # 64-block (1,024-token) work items
+                                                (kv.KVShape(2, 8, 128, 16), 40, 20, 3000),
+                                                (kv.KVShape(2, 8, 128, 16), 40, 24, 6000)])
+def test_attention_vs_oracle_ragged(shape, hq, S, maxlen):
+    """Ragged lengths (0, 1, d-1, d, d+1, 255-257 chunk edges, work-item edges 511-513 / 1023-1025 /
+    2047-2049, random up to maxlen) through a shuffled block table; GQA groups of 5, 4 and 4. The
+    host picks the work item (16 / 32 / 64 blocks) from the grid size: the last two cases take 32
+    and 64."""
     torch = _torch()
     from paper_2507_21433_b200 import _lib as L
-    rng = np.random.default_rng(hq)
-    S = 12
-    seq_len = sd.ragged_lengths(rng, S, 3000)
-    stride = int(math.ceil(3000 / 16)) + 1
+    rng = np.random.default_rng(hq + S + maxlen)
+    seq_len = sd.ragged_lengths(rng, S, maxlen)
+    edges = [511, 512, 513, 1023, 1024, 1025, 2047, 2048, 2049]
+    if S >= 8 + len(edges):                      # after ragged_lengths' own 8 edge lengths
+        seq_len[8:8 + len(edges)] = edges
+    stride = int(math.ceil(maxlen / 16)) + 1
     need = [int(math.ceil(n / 16)) for n in seq_len]
     nb = sum(need) + 5
     perm = rng.permutation(nb)
