@@ -840,19 +840,23 @@ __device__ void s1_item(const CandArgs& a, SelSmem<NT>& sm, int64_t wi, int64_t 
   int4& s_lb = *s_lb_p;
   auto publish_nothing = [&](int64_t key) { s1_publish_nothing<NT>(a, key, nwork, s_lb_p); };
   const int64_t k = g - gfirst;
+  // every per-step value the item needs, issued together before the first branch (one memory
+  // latency instead of a chain: the branch on nbag kept the compiler from hoisting the others)
   const int32_t nbag = a.step_nbag[g];
+  const int64_t tok_base = a.seq_tok_off[s];
+  const int32_t st_start = a.step_start[g], st_end = a.step_end[g];
+  const int64_t n2_raw = a.ws.n2[g];
   if (nbag == 0 || !is_current(a, s, k, S)) {
     if (crank == 0 && threadIdx.x == 0) { a.ws.cnt_m[g] = 0; a.ws.cnt_t[g] = 0; a.ws.cnt_p[g] = 0; a.ws.stash_base[g] = 0; }
     if (fused && crank == 0) publish_nothing(wi);
     return;
   }
-  const int64_t tok_base = a.seq_tok_off[s];
   const int32_t* t = a.tokens + tok_base;
-  const Table tb = build_table(a, sm.tab, t, tok_base, a.step_start[g], a.step_end[g], nbag, S1Cfg<NT>::kSlots,
+  const Table tb = build_table(a, sm.tab, t, tok_base, st_start, st_end, nbag, S1Cfg<NT>::kSlots,
                                sm.u.bm, crank == 0);
   if (tb.global && csize > 1) cl.sync();                 // rank 0 filled the shared global table
   DBG_T(1);
-  const double n2k = (double)a.ws.n2[g];
+  const double n2k = (double)n2_raw;
   if (threadIdx.x == 0) { sm.count = 0; sm.overflow = 0; }
   __syncthreads();
   const bool compact = a.top_k > 0 && a.top_k <= kCandCap / 2;
@@ -1086,7 +1090,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
   // and which never wait on larger ones, so progress does not depend on how many CTAs (or
   // clusters) are co-resident (a static map deadlocks when fewer fit than were launched).
   __shared__ unsigned long long s_ticket;
-  for (;;) {
+  for (bool first = true;; first = false) {
     int64_t wi;
     if (csize == 1) {
       __syncthreads();                                     // everyone has read the previous ticket
@@ -1094,7 +1098,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
       __syncthreads();
       wi = (int64_t)s_ticket;
     } else {
-      cl.sync();                                           // every rank has read rank 0's previous ticket
+      // every rank has read rank 0's previous ticket (none before the first: the barrier below
+      // alone orders rank 0's write before the remote reads)
+      if (!first) cl.sync();
       if (crank == 0 && threadIdx.x == 0) s_ticket = atomicAdd(a.ws.ticket, 1ull);
       cl.sync();
       wi = (int64_t)*cl.map_shared_rank(&s_ticket, 0);
