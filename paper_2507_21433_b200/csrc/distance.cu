@@ -43,9 +43,6 @@ constexpr int kPhi4Slice = 40960;
 constexpr int kRingBytes = 224 * 1024;                      // shared-memory ring (of 227 KB per CTA)
 constexpr int kMaxKre = 10;                                 // largest stage: 40 KiB (one Phi-4 slice)
 constexpr int kMaxRingStages = 48;
-#ifndef MS_ST_PAIRRED
-#define MS_ST_PAIRRED 0      // tuning: paired warp reductions in the Euclidean consumer
-#endif
 #ifndef MS_ST_MAXKRE
 #define MS_ST_MAXKRE kMaxKre      // tuning: cap on the stage size, in 4 KiB units
 #endif
@@ -555,70 +552,6 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) distance_st_kernel(DistArgs a
   if (ha.w & H_STOP) return;
   load(xa, ha.z);
   release();
-#if MS_ST_PAIRRED
-  if (MET == MEMSHARE_METRIC_EUCLIDEAN) {
-    // Euclidean: the lane partials of TWO consecutive stages are reduced together (one transposed
-    // butterfly: lanes 0-15 carry the first stage's sum, 16-31 the second's -- 5 shuffles for two
-    // warp sums instead of 10); an anchor stage contributes no partial
-    auto part = [&](int4 h, const uint4 (&x)[KRE]) -> float {
-      if (h.w & H_ANCHOR) {
-#pragma unroll
-        for (int r = 0; r < KRE; ++r) {
-          T[4 * r + 0] = bf2_to_f2(x[r].x);
-          T[4 * r + 1] = bf2_to_f2(x[r].y);
-          T[4 * r + 2] = bf2_to_f2(x[r].z);
-          T[4 * r + 3] = bf2_to_f2(x[r].w);
-        }
-        return 0.f;
-      }
-      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int r = 0; r < KRE; ++r) {
-        const float2 d0 = sub_bf2(x[r].x, T[4 * r + 0]);
-        const float2 d1 = sub_bf2(x[r].y, T[4 * r + 1]);
-        const float2 d2 = sub_bf2(x[r].z, T[4 * r + 2]);
-        const float2 d3 = sub_bf2(x[r].w, T[4 * r + 3]);
-        acc0 = __ffma2_rn(d0, d0, acc0);
-        acc1 = __ffma2_rn(d1, d1, acc1);
-        acc0 = __ffma2_rn(d2, d2, acc0);
-        acc1 = __ffma2_rn(d3, d3, acc1);
-      }
-      return (acc0.x + acc0.y) + (acc1.x + acc1.y);
-    };
-    auto out_of = [](int4 h) { return (int64_t)(((uint64_t)(uint32_t)h.y << 32) | (uint32_t)h.x); };
-    auto store2 = [&](int4 h0, float v0, int4 h1, float v1) {
-      const bool hi = lane & 16;
-      float k = hi ? v1 : v0;
-      k += __shfl_xor_sync(0xffffffffu, hi ? v0 : v1, 16);
-      k += __shfl_xor_sync(0xffffffffu, k, 8);
-      k += __shfl_xor_sync(0xffffffffu, k, 4);
-      k += __shfl_xor_sync(0xffffffffu, k, 2);
-      k += __shfl_xor_sync(0xffffffffu, k, 1);
-      if (lane == 0 && (h0.w & H_PAIR)) a.ws.wpart[out_of(h0) + warp] = k;
-      if (lane == 16 && (h1.w & H_PAIR)) a.ws.wpart[out_of(h1) + warp] = k;
-    };
-    for (;;) {
-      mbar_wait(&sm.full[stage], ph);
-      hb = sm.hdr[stage];
-      if (!(hb.w & H_STOP)) load(xb, hb.z);
-      const float va = part(ha, xa);
-      if (hb.w & H_STOP) {
-        store2(ha, va, hb, 0.f);
-        break;
-      }
-      release();
-      const int4 h0 = ha;
-      mbar_wait(&sm.full[stage], ph);
-      ha = sm.hdr[stage];
-      if (!(ha.w & H_STOP)) load(xa, ha.z);
-      const float vb = part(hb, xb);
-      store2(h0, va, hb, vb);
-      if (ha.w & H_STOP) break;
-      release();
-    }
-    return;
-  }
-#endif
   for (;;) {
     mbar_wait(&sm.full[stage], ph);
     hb = sm.hdr[stage];
