@@ -219,7 +219,10 @@ size_t memshare_step_candidates_workspace_size(int64_t num_tokens, int32_t num_s
  *   pool, dims (host structs)     geometry; pool unused in FINALIZE mode
  *   pairs, target_off, num_pairs, num_targets   memshare_step_candidates outputs (device);
  *                                 counts are clamped to pair_cap / target_cap
- *   mode FULL | PARTIAL | FINALIZE; metric EUCLIDEAN | COSINE (COSINE: FULL mode only)
+ *   mode FULL | PARTIAL | FINALIZE, optionally | MEMSHARE_DIST_GROUPED (schedule hint, see its
+ *                                 definition); metric EUCLIDEAN | COSINE (COSINE: FULL mode only)
+ *   workspace                     >= memshare_block_distance_workspace_size(); caller-owned, no
+ *                                 initial contents required (every call resets what it uses)
  *   partial_sq float [pair_cap][N][2]   PARTIAL: output (sum over local heads of squared
  *                                 differences, [.][l][0] = K, [.][l][1] = V); FINALIZE: input;
  *                                 FULL: optional output (may be NULL)
@@ -375,8 +378,9 @@ size_t memshare_kv_append_workspace_size(int32_t num_seqs);
  *   max_seq_len     host upper bound of seq_len (sizes the split-KV grid and the workspace);
  *                   table_stride >= ceil(max_seq_len / 16)
  *   out             fp32 [num_seqs][num_q_heads][head_dim] (device)
- * Implementation: split-KV over 256-token chunks (one CTA per chunk x KV head x sequence, fp32
- * online softmax), then one warp per (sequence, query head) combines the chunks. A table entry
+ * Implementation: split-KV over chunks of 1,024 / 512 / 256 tokens -- the largest that still gives
+ * >= 4 CTAs per SM (one CTA per chunk x KV head x sequence, fp32 online softmax) -- then one warp
+ * per (sequence, query head) combines the chunks. A table entry
  * outside [0, num_blocks) sets CORRUPTION. Host errors: INVALID_ARGUMENT. */
 memshare_status memshare_paged_attention_decode(const memshare_kv_pool* pool_host, const memshare_dims* dims_host,
                                                 int32_t layer, const void* q, int32_t num_q_heads,
