@@ -1040,14 +1040,13 @@ __device__ void s1_item(const CandArgs& a, SelSmem<NT>& sm, int64_t wi, int64_t 
 // run once per launch, instruction-fetch sensitive -- as small as before)
 template <int NT, bool RI = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) stage1_kernel(CandArgs a) {
-  constexpr int kNTs = NT, kNWs = NT / 32;
+  constexpr int kNTs = NT;
   static_assert(NT != 1024 || kMaxTgt * 16 <= S1Cfg<1024>::kTok * 4, "fused fill reuses the staging area");
   const bool fused = NT == 1024 && a.fused != 0;   // the 512-thread shape never fuses
   pdl_trigger();
   TL_SCOPE(3);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SelSmem<NT>& sm = *reinterpret_cast<SelSmem<NT>*>(smem_raw);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // Thread-block cluster of csize CTAs per current step (online rounds: few current steps, long
   // histories): every rank builds the step's table, streams 1/csize of the history into its own
   // shared dot array, and rank 0 sums the ranks' arrays over DSMEM and does the selection.

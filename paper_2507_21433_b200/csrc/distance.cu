@@ -747,6 +747,10 @@ __device__ __forceinline__ void grp_producer(GrpSmem<KRE>& sm, const DistArgs& a
   }
 }
 
+#ifndef MS_GRP_F32
+#define MS_GRP_F32 1
+#endif
+#if !MS_GRP_F32
 // e = RN(s - t) for a packed pair of anchor elements (bf16 halves of `t2`) and two fp32 sources
 __device__ __forceinline__ float2 rsub_bf2(uint32_t t2, float s0, float s1) {
   float2 d;
@@ -756,10 +760,8 @@ __device__ __forceinline__ float2 rsub_bf2(uint32_t t2, float s0, float s1) {
       : "r"(t2), "f"(s0), "f"(s1), "h"((unsigned short)0xBF80u));
   return d;
 }
-
-#ifndef MS_GRP_F32
-#define MS_GRP_F32 1
 #endif
+
 #if MS_GRP_F32
 // anchors held NEGATED in fp32 (the consumer warpgroups own 216 registers, setmaxnreg): e = s + (-t)
 // = RN(s - t) by one FADD2 per two elements, the same value as the FHFMA form
