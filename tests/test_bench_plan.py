@@ -71,3 +71,23 @@ def test_two_ranks_take_disjoint_shares_of_the_same_plan():
         flat = sorted(i for share in got for wave in share for i in wave)
         assert flat == list(range(64))
         assert ms == 2.0 and pairs == 300.0                   # max over ranks of the step time; sum of pairs
+
+
+def test_dual_ceiling_picks_the_binding_bound():
+    """roofline.dual: distinct bytes against the HBM peak vs staged (T + P) slice bytes against the
+    L2 -> shared-memory rate; the larger time is the bound and frac_of_bound its fraction."""
+    peak = bench.measured_peaks()[0]
+    blk = 4 << 20                                             # one 32B-shape block, all layers, K and V
+    # low sharing: (T + P) / U = 1.5 -> the HBM time is the larger one
+    U, T, P = 1000, 500, 1000
+    t_hbm = U * blk / (peak * 1e9)
+    d = bench.dual_ceiling(U, T, P, U * blk, 1e3 * t_hbm / 0.9)
+    assert d["bound"] == "hbm" and abs(d["frac_of_bound"] - 0.9) < 1e-9
+    assert d["staged_bytes"] == (T + P) * blk and abs(d["staged_over_distinct"] - 1.5) < 1e-12
+    # heavy sharing: (T + P) / U = 4 -> the staged bytes bind
+    T, P = 1000, 3000
+    t_l2 = (T + P) * blk / (bench.L2_DELIVERY_GBS * 1e9)
+    assert t_l2 > t_hbm
+    d = bench.dual_ceiling(U, T, P, U * blk, 1e3 * t_l2 / 0.5)
+    assert d["bound"] == "l2_delivery" and abs(d["frac_of_bound"] - 0.5) < 1e-9
+    assert abs(d["l2_frac"] - 0.5) < 1e-9
