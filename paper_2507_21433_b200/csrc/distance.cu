@@ -156,7 +156,13 @@ __device__ __forceinline__ int64_t clamp_count(const int64_t* p, int64_t cap) {
 __device__ __forceinline__ int32_t unit_lpi(const DistArgs& a) {
   if (!a.lpi_auto || a.lpi <= 1) return a.lpi;
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
-  return T * (int64_t)a.n_chunks < 2 * (int64_t)gridDim.x ? 1 : a.lpi;
+  if (T * (int64_t)a.n_chunks < 2 * (int64_t)gridDim.x) return 1;
+  // long lists of 32 KiB slices (the 32B shapes' batch waves) take 3-layer units: same-box A/B, c3
+  // (64 sequences) 13.61 vs 13.74-13.85 ms per step, c5 (32) 9.66-9.73 vs 9.73-9.77 ms; 40 KiB
+  // (Phi-4) slices and short lists (a single CoT: c2, 145 targets) stay at 2 (lpi 3 measured
+  // 5 % slower on c4, 1 % on c2)
+  if (a.lpi == 2 && a.slice_bytes == 32768 && a.n_sub == 1 && T >= 1024 && a.N >= 6) return 3;
+  return a.lpi;
 }
 
 // fixed-order fp32 sum of the per-warp partials of (row, layer l, kv) of one workspace buffer
