@@ -989,14 +989,32 @@ __global__ void ticket_reset_kernel(unsigned int* ticket) {
   if (threadIdx.x < 2) ticket[threadIdx.x] = 0u;          // the unit ticket and the finalize CTA count
 }
 
+// last_block_done over the first `n` CTAs of the grid
+__device__ __forceinline__ bool last_of(unsigned int* ctr, unsigned n) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ctr, 1u) == n - 1;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(DistArgs a, int from_partial) {
   pdl_trigger();
   TL_SCOPE(7);
   __shared__ double terms[kFinThreads];
   const int64_t T = clamp_count(a.num_targets, a.target_cap);
+  // the grid is sized from target_cap on the host; CTAs beyond the device count leave at once and
+  // do not take part in the fused remap's last-CTA election (an online round's few targets on a
+  // large cap: one atomic per working CTA, not per launched CTA)
+  const unsigned active = (unsigned)(T < 1 ? 1 : (T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x));
+  if (blockIdx.x >= active) return;
   for (int64_t t = blockIdx.x; t < T; t += gridDim.x)
     finalize_target(a, t, terms, threadIdx.x, from_partial != 0, [] { __syncthreads(); });
-  if (a.remap && last_block_done(a.ws.fin_done)) {
+  if (a.remap && last_of(a.ws.fin_done, active)) {
     // a7 fused: every decision is written (each CTA's writes precede its count, last_block_done)
     __shared__ int64_t rsh[kFinThreads / 32 + 1];
     __shared__ int rbad;
